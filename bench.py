@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark: FAST-HALS iterations/sec on the 20News-shaped sparse A at K=240
+(BASELINE.json metric; configs[1] = SURVEY.md C2), PL-NMF tiled algorithm,
+fp64, on the B200 engine.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+
+A step is one FAST-HALS iteration (R=A^T W, S=W^T W, H update, P=A Ht,
+Q=Ht^T Ht, W update) with everything resident in HBM.  Each step is timed
+with CUDA events on the engine stream; L2 is flushed (a 512 MiB write) between
+steps, outside the timed interval.  N>1 runs N independent replicas (one
+process per GPU; C2 does not shard) and reports the max over
+ranks.  One JSON line is printed by rank 0.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+libplnmf compiled from the unmodified sources) on this host's cores, same
+workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# C2 of SURVEY.md 8(d): 20News shape, nnz ~ 1,018,191, K=240.
+V, D, NNZ_TARGET, K = 26214, 11314, 1018191, 240
+DENSITY = NNZ_TARGET / (V * D)
+GEN_SEED = 20
+TILE = 16  # T_auto of the reference's cost model for K=240 (best_integer_tile), BASELINE.md 2
+METRIC = "FAST-HALS iters/sec at K=240 (20News-shaped sparse A); SpMM % HBM peak"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_input():
+    from paper_1904_07935_b200 import plnmf as P
+    return P.synth_csr(V, D, DENSITY, GEN_SEED)
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return rank, world, local, dist
+    return rank, world, local, None
+
+
+def allmax(dist, local, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def time_reference_cpu(m, steps, warmup, tiled=True, iters_per_step=1):
+    """The reference's iterate() (oracle/_ref) on this host's cores; s/iter with
+    the reference's convention (total - error_eval) / iters (acceptance.cpp:251)."""
+    from oracle.oracle import RefInput, ref, ref_init_factors, ref_iterate
+    a = RefInput(m.rows, m.cols, m.row_ptr, m.col_idx, m.values)
+    w, ht = ref_init_factors(m.rows, m.cols, K, seed=0)
+    cores = ref().ref_max_threads()
+    per = []
+    for i in range(warmup + steps):
+        # continue the trajectory step by step; error evaluated once per call
+        w, ht, tr = ref_iterate(a, w, ht, K, max_iters=iters_per_step, rel_tol=0.0, error_every=iters_per_step,
+                                tile=TILE if tiled else 0, tiled=tiled)
+        if i >= warmup:
+            per.append((tr["total_seconds"] - tr["totals"][8]) / iters_per_step)
+    return per, cores
+
+
+def reference_arm(args):
+    rank, world, local, dist = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    m = make_input()
+    try:
+        per, cores = time_reference_cpu(m, args.steps, args.warmup, tiled=True)
+    except ImportError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return
+    spi = float(np.mean(per))
+    val = 1.0 / spi
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": spi * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(m),
+        "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} PL-NMF iterations (T={TILE}) of C2 after {args.warmup} warm-up, "
+                                   "reference iterate() compiled from /root/reference sources, OpenMP on all host cores"},
+        "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(m):
+    return {"workload": f"C2: 20News-shaped synthetic CSR {V}x{D}, nnz={m.nnz()}, K={K}, PL-NMF tile {TILE}, "
+                        "FAST-HALS iteration (H then W update)",
+            "V": V, "D": D, "nnz": m.nnz(), "K": K, "tile_size": TILE, "algorithm": "pl-nmf (tiled)",
+            "generator": f"splitmix64 geometric-gap Bernoulli rows, seed {GEN_SEED}, values U(0.1,2.0) fp32-rounded",
+            "l2": "flushed (512 MiB write) between timed steps"}
+
+
+# ----------------------------------------------------------------------------- engine arm
+def spmm_bytes(rows, other_rows, nnz, k):
+    """Algorithmic HBM bytes of one fp64 CSR SpMM launch: values (8 B) + int32
+    column indices (4 B) per nonzero, int64 row pointers, the dense operand read
+    once and the output written once."""
+    return 12 * nnz + 8 * (rows + 1) + 8 * other_rows * k + 8 * rows * k
+
+
+def engine_arm(args):
+    import torch
+    from paper_1904_07935_b200 import plnmf as P
+
+    rank, world, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    m = make_input()
+    a = P.InputMatrix(m)
+    eng = P.Engine(a, K, device=local)
+    eng.set_math(P.Math.exact if args.math == "exact" else P.Math.fused)
+    cfg = P.SolverConfig(rank=K, tile_size=TILE, max_iters=1, rel_tol=0.0, seed=rank)
+    alg = P.Algorithm.tiled
+    eng.init_factors(cfg)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    for _ in range(args.warmup):
+        eng.run_iterations(cfg, alg, 1)
+    launches0 = eng.stats()["kernel_launches"]
+    step_ms = []
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            step_ms.append(eng.run_iterations(cfg, alg, 1))
+    torch.cuda.synchronize()
+    barrier(dist)
+    launches = eng.stats()["kernel_launches"] - launches0
+    total_ms = allmax(dist, local, float(sum(step_ms)))
+    value = world * args.steps / (total_ms * 1e-3)
+
+    # back-to-back (L2 warm) for context
+    eng.run_iterations(cfg, alg, 2)
+    warm_ms = allmax(dist, local, eng.run_iterations(cfg, alg, args.steps)) / args.steps
+
+    # per-kernel times (CUDA events on the engine stream) for the roofline
+    reps = 10
+    kt = {"spmm_A_Ht": eng.time_kernel(cfg, 0, reps), "spmm_At_W": eng.time_kernel(cfg, 1, reps),
+          "gram_W": eng.time_kernel(cfg, 2, reps), "update_w_tiled": eng.time_kernel(cfg, 3, reps),
+          "update_h_tiled": eng.time_kernel(cfg, 4, reps)}
+    pk = peaks()
+    hbm = float(pk["hbm_gbs"])
+    nnz = m.nnz()
+    b_p = spmm_bytes(V, D, nnz, K)
+    b_r = spmm_bytes(D, V, nnz, K)
+    step = total_ms / args.steps
+    # dominant kernel by share of the step (two SpMMs per step)
+    shares = {"spmm": kt["spmm_A_Ht"] + kt["spmm_At_W"], "update_w_tiled": kt["update_w_tiled"],
+              "update_h_tiled": kt["update_h_tiled"], "gram": 2 * kt["gram_W"]}
+    # W update algorithmic bytes: read W, P, write+read the accumulator, write W_new
+    b_w = 8 * V * K * 4 + 8 * K * K
+    rl_spmm = b_p / (kt["spmm_A_Ht"] * 1e-3) / 1e9
+    roofline = {"kernel": "spmm_csr A*Ht (K1)", "bound": "hbm", "achieved": rl_spmm, "peak": hbm, "unit": "GB/s",
+                "frac": rl_spmm / hbm, "traffic": ncu_traffic("spmm_csr"),
+                "algorithmic_bytes": b_p, "launch_ms": kt["spmm_A_Ht"],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback"}
+    # e2e through the reference-facing C-ABI call with host factors
+    e2e = e2e_arm(P, a, eng, cfg, alg, args, torch)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            per, cores = time_reference_cpu(m, steps=args.cpu_steps, warmup=1, tiled=True)
+            cpu = {"value": 1.0 / float(np.mean(per)), "unit": "iters/s", "cores": cores, "kind": "reference",
+                   "sample": f"{args.cpu_steps} PL-NMF iterations (T={TILE}) of C2 after 1 warm-up, reference "
+                             "iterate() (oracle/_ref, compiled from the reference sources), all host cores"}
+        except ImportError as e:
+            cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(m),
+            "math": args.math, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "warm_l2_ms_per_iter": warm_ms,
+            "kernels_ms": kt, "kernel_share_of_step": {k2: v2 / step for k2, v2 in shares.items()},
+            "spmm_roofline": {"A_Ht_GBps": rl_spmm, "At_W_GBps": b_r / (kt["spmm_At_W"] * 1e-3) / 1e9,
+                              "bytes_A_Ht": b_p, "bytes_At_W": b_r,
+                              "l2_gather_bytes": 8 * nnz * K},
+            "update_w_bytes": b_w,
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_arm(P, a, eng, cfg, alg, args, torch):
+    """Each step = one drop-in iterate() call through the C-ABI with HOST
+    factors (plnmf_gpu_iterate_host): H2D of W and Ht, one FAST-HALS iteration
+    with the reference's error evaluations, D2H of W, Ht and the trace."""
+    import ctypes as C
+    from paper_1904_07935_b200 import _lib as L
+    f = eng.get_factors()
+    w = np.asfortranarray(f.w)
+    ht = np.asfortranarray(f.ht)
+    c = cfg.to_c()
+    buf = P._TraceBuf(1)
+    lib = L.lib()
+    ptr = lambda x: x.ctypes.data_as(L.P_f64)  # noqa: E731
+    for _ in range(2):
+        P._check(lib.plnmf_gpu_iterate_host(eng._h, C.byref(c), int(alg), ptr(w), ptr(ht), C.byref(buf.c)))
+    t0 = time.perf_counter()
+    n = max(3, args.steps // 2)
+    for _ in range(n):
+        P._check(lib.plnmf_gpu_iterate_host(eng._h, C.byref(c), int(alg), ptr(w), ptr(ht), C.byref(buf.c)))
+    dt = time.perf_counter() - t0
+    fb = 8 * (V + D) * K
+    return {"value": n / dt, "unit": "iters/s", "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb + 8 * 3,
+            "what": "plnmf_gpu_iterate_host(max_iters=1): upload W,Ht (col-major f64), iterate incl. the "
+                    "reference's initial + final error evaluation, download W,Ht; host wall clock"}
+
+
+def ncu_traffic(kernel):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--math", default="exact", choices=["exact", "fused"])
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        engine_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * plnmf_gpu.h — C-ABI of the B200-native FAST-HALS / PL-NMF engine.
+ *
+ * This is the drop-in boundary for the reference's iteration loop
+ * (arxiv/paper_1904_07935, /root/reference/proj).  Every entry point names the
+ * reference interface it replaces.  Only plain pointers, sizes and PODs cross
+ * it; matrices cross it exactly as the reference stores them: fp64,
+ * column-major, element (r, c) at data[r + c*rows]
+ * (proj/include/plnmf/dense_matrix.hpp:33-35), CSR with int64 indices
+ * (proj/include/plnmf/csr_matrix.hpp:10-21).  Inside the engine the factors
+ * live on the GPU row-major; the layout is converted only here.
+ *
+ * Errors: every call returns a plnmf_status; the message of the last failing
+ * call on the calling thread is plnmf_last_error().  The status codes map 1:1
+ * onto the reference's exception types:
+ *   PLNMF_INVALID_ARGUMENT  std::invalid_argument  (config, shape, tile)
+ *   PLNMF_RUNTIME           std::runtime_error     (non-finite objective)
+ *   PLNMF_DOMAIN            std::domain_error      (||A|| = 0)
+ *   PLNMF_CUDA              CUDA failure (no reference counterpart)
+ *
+ * Threading: one engine = one CUDA device + one stream; an engine is not
+ * thread-safe, distinct engines are (proj/tools/plnmf.cpp:104-106).
+ */
+#ifndef PLNMF_GPU_H
+#define PLNMF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLNMF_GPU_ABI_VERSION 1
+
+typedef enum plnmf_status {
+    PLNMF_OK = 0,
+    PLNMF_INVALID_ARGUMENT = 1,
+    PLNMF_RUNTIME = 2,
+    PLNMF_DOMAIN = 3,
+    PLNMF_CUDA = 4,
+    PLNMF_NCCL = 5
+} plnmf_status;
+
+/* proj/include/plnmf/config.hpp:9 — Algorithm{reference, tiled}
+ * ("fast-hals" / "pl-nmf" on the CLI, proj/tools/plnmf.cpp:76-80). */
+typedef enum plnmf_algorithm { PLNMF_ALGORITHM_REFERENCE = 0, PLNMF_ALGORITHM_TILED = 1 } plnmf_algorithm;
+
+/* Arithmetic of the device kernels. EXACT performs every multiply and add
+ * separately, round-to-nearest, in the reference's per-element order (no FMA
+ * contraction — the reference Release build has none).  FUSED uses fma() in
+ * the same order (one rounding per multiply-add). */
+typedef enum plnmf_math { PLNMF_MATH_EXACT = 0, PLNMF_MATH_FUSED = 1 } plnmf_math;
+
+/* proj/include/plnmf/config.hpp:11-22 — SolverConfig, field for field. */
+typedef struct plnmf_config {
+    int64_t rank;        /* K, >= 1 */
+    double epsilon;      /* clamp floor, > 0 (default 1e-16) */
+    int64_t max_iters;   /* >= 0 (default 100) */
+    double rel_tol;      /* >= 0 (default 1e-6) */
+    uint64_t seed;       /* default 0 */
+    int64_t error_every; /* >= 1 (default 1) */
+    int32_t deterministic; /* accepted, as in the reference (never read by its kernels);
+                              the device kernels are run-to-run deterministic regardless */
+    int64_t tile_size;   /* 0 = unresolved; the tiled path needs [1, rank] */
+} plnmf_config;
+
+/* proj/include/plnmf/workspace.hpp:15-28 — PhaseTimes (seconds). */
+typedef struct plnmf_phase_times {
+    double precompute_h, update_h, precompute_w, update_w;
+    double phase1, phase2, phase3, normalize, error_eval;
+} plnmf_phase_times;
+
+/* proj/include/plnmf/solver.hpp:12-17 — TraceRecord. */
+typedef struct plnmf_trace_record {
+    int64_t iteration;
+    double rel_error;
+    double elapsed_s;
+    plnmf_phase_times phases;
+} plnmf_trace_record;
+
+/* proj/include/plnmf/solver.hpp:19-25 — ConvergenceTrace.  The caller owns
+ * `records` (capacity >= max_iters); n_records is filled in. */
+typedef struct plnmf_trace {
+    double initial_error;
+    double total_seconds;
+    uint64_t update_macs;
+    plnmf_phase_times totals;
+    int64_t n_records;
+    int64_t capacity;
+    plnmf_trace_record* records;
+} plnmf_trace;
+
+/* Workspace products (proj/include/plnmf/workspace.hpp:39-55). */
+typedef enum plnmf_product {
+    PLNMF_PRODUCT_P = 0,  /* A * Ht     V x K */
+    PLNMF_PRODUCT_Q = 1,  /* Ht^T * Ht  K x K */
+    PLNMF_PRODUCT_R = 2,  /* A^T * W    D x K */
+    PLNMF_PRODUCT_S = 3,  /* W^T * W    K x K */
+    PLNMF_PRODUCT_COLUMN_NORMS = 4 /* K, last W-update pre-normalisation norms */
+} plnmf_product;
+
+typedef struct plnmf_gpu_engine plnmf_gpu_engine;
+
+/* Engine counters (instrumentation; no reference counterpart). */
+typedef struct plnmf_gpu_stats {
+    uint64_t kernel_launches;  /* engine kernels launched since create / reset */
+    int32_t persistent_ctas;   /* CTAs of the grid-synchronised W update */
+    int32_t sm_count;
+    int64_t device_bytes;      /* device memory held by the engine */
+} plnmf_gpu_stats;
+
+/* ---- host-side helpers (no GPU needed) --------------------------------------- */
+const char* plnmf_last_error(void);
+int32_t plnmf_gpu_abi_version(void);
+/* SolverConfig defaults (config.hpp:11-22) and SolverConfig::validate (config.cpp:7-15). */
+void plnmf_config_default(plnmf_config* cfg);
+plnmf_status plnmf_config_validate(const plnmf_config* cfg);
+/* plan_tiles (proj/src/tiling.cpp:8-18); begins/ends may be NULL to query gamma. */
+plnmf_status plnmf_plan_tiles(int64_t k, int64_t tile_size, int64_t* begins, int64_t* ends,
+                              int64_t* gamma);
+/* init_factors (proj/src/solver.cpp:43-51): mt19937_64, bit-identical to the reference. */
+plnmf_status plnmf_init_factors(int64_t v, int64_t d, const plnmf_config* cfg, double* w_colmajor,
+                                double* ht_colmajor);
+/* Synthetic non-negative CSR: row r has Bernoulli(density) cells
+ * at distinct sorted columns (geometric gaps from a counter-based splitmix64
+ * stream keyed by (seed, r)), values U(0.1, 2.0) rounded to fp32.  Two calls:
+ * with col_idx == NULL fills row_ptr (rows+1) and *nnz; then fills col_idx/values. */
+plnmf_status plnmf_synth_csr(int64_t rows, int64_t cols, double density, uint64_t seed,
+                             int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz);
+
+/* ---- engine -------------------------------------------------------------------- */
+int32_t plnmf_gpu_device_count(void);
+
+/* Uploads A (InputMatrix, proj/include/plnmf/input_matrix.hpp:11-34): validates
+ * like CsrMatrix::validate (proj/src/csr_matrix.cpp:8-28), caches ||A||_F^2 in the
+ * reference's serial order (proj/src/input_matrix.cpp:15-20), and builds A^T on
+ * the device once (the reference caches transpose(A) in ws.at, proj/src/hals.cpp:26). */
+plnmf_status plnmf_gpu_create_csr(int32_t device, int64_t rows, int64_t cols, int64_t nnz,
+                                  const int64_t* row_ptr, const int64_t* col_idx,
+                                  const double* values, int64_t rank, plnmf_gpu_engine** out);
+plnmf_status plnmf_gpu_create_dense(int32_t device, int64_t rows, int64_t cols,
+                                    const double* a_colmajor, int64_t rank,
+                                    plnmf_gpu_engine** out);
+plnmf_status plnmf_gpu_destroy(plnmf_gpu_engine* e);
+/* InputMatrix::norm_sq / nnz / rows / cols (input_matrix.hpp:17-28). */
+plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int64_t* cols,
+                                  int64_t* nnz, double* norm_sq);
+plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math);
+
+/* FactorPair in/out (proj/include/plnmf/workspace.hpp:32-35). */
+plnmf_status plnmf_gpu_set_factors(plnmf_gpu_engine* e, const double* w_colmajor,
+                                   const double* ht_colmajor);
+plnmf_status plnmf_gpu_get_factors(plnmf_gpu_engine* e, double* w_colmajor, double* ht_colmajor);
+/* init_factors on the host (bit-identical) followed by set_factors. */
+plnmf_status plnmf_gpu_init_factors(plnmf_gpu_engine* e, const plnmf_config* cfg);
+
+/* iterate (proj/src/solver.cpp:53-115): same loop, cadence, stop rule, trace and
+ * exceptions, on the device-resident factors.  trace may be NULL. */
+plnmf_status plnmf_gpu_iterate(plnmf_gpu_engine* e, const plnmf_config* cfg,
+                               plnmf_algorithm algorithm, plnmf_trace* trace);
+
+/* One-call drop-in for iterate() on HOST factors: uploads W/Ht, iterates,
+ * downloads them back in place (what `Algorithm::gpu` in solver.cpp binds to). */
+plnmf_status plnmf_gpu_iterate_host(plnmf_gpu_engine* e, const plnmf_config* cfg,
+                                    plnmf_algorithm algorithm, double* w_colmajor,
+                                    double* ht_colmajor, plnmf_trace* trace);
+
+/* ---- step API (proj/include/plnmf/hals.hpp:11-21, tiled.hpp:37-40) ----------- */
+plnmf_status plnmf_gpu_precompute_h_products(plnmf_gpu_engine* e); /* R = A^T W, S = W^T W */
+plnmf_status plnmf_gpu_precompute_w_products(plnmf_gpu_engine* e); /* P = A Ht,  Q = Ht^T Ht */
+plnmf_status plnmf_gpu_update_h(plnmf_gpu_engine* e, const plnmf_config* cfg,
+                                plnmf_algorithm algorithm);
+plnmf_status plnmf_gpu_update_w(plnmf_gpu_engine* e, const plnmf_config* cfg,
+                                plnmf_algorithm algorithm);
+/* evaluate_error (proj/src/solver.cpp:32-39): S = gram(W), Gram identity
+ * (metrics.cpp:94-127), direct fallback below 1e-6 (metrics.cpp:79-92).
+ * out3 = {frobenius_sq, relative, cancellation}. */
+plnmf_status plnmf_gpu_evaluate_error(plnmf_gpu_engine* e, double* out3);
+/* relative_error_direct (proj/src/metrics.cpp:79-92); out2 = {frobenius_sq, relative}. */
+plnmf_status plnmf_gpu_relative_error_direct(plnmf_gpu_engine* e, double* out2);
+plnmf_status plnmf_gpu_get_product(plnmf_gpu_engine* e, plnmf_product which, double* out_colmajor);
+plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which,
+                                   const double* in_colmajor);
+
+/* ---- timing / instrumentation --------------------------------------------------- */
+/* n full iterations (H then W update, no error evaluation, no host sync inside),
+ * timed with CUDA events on the engine stream; *device_ms = total. */
+plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* cfg,
+                                      plnmf_algorithm algorithm, int64_t n, double* device_ms);
+/* Times `reps` launches of one engine kernel family on the current state:
+ * 0 = SpMM A*Ht (P), 1 = SpMM A^T*W (R), 2 = gram(W), 3 = W update, 4 = H update.
+ * *avg_ms = mean CUDA-event duration per launch (events on the engine stream). */
+plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg, int32_t which,
+                                   int32_t reps, double* avg_ms);
+plnmf_status plnmf_gpu_get_stats(const plnmf_gpu_engine* e, plnmf_gpu_stats* out);
+plnmf_status plnmf_gpu_synchronize(plnmf_gpu_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLNMF_GPU_H */

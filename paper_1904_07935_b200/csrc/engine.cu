@@ -1,0 +1,784 @@
+// The engine: device-resident A (CSR + CSR of A^T, or dense), factors and
+// workspace, the iteration loop of proj/src/solver.cpp:53-115, the step API of
+// proj/include/plnmf/hals.hpp / tiled.hpp, and the C-ABI over it.
+//
+// One engine = one device + two streams (the main stream runs the chain; the
+// side stream runs the Gram product concurrently with the SpMM that reads the
+// same factor).  All host<->device traffic happens at the boundary
+// (create / set / get); the loop itself only reads back the 3-double error
+// report when the objective is evaluated.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+#include "plnmf_gpu.h"
+
+using plnmf::Math;
+namespace kern = plnmf::kern;
+
+struct plnmf_gpu_engine {
+    int device = 0;
+    cudaStream_t s = nullptr, s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int64_t v = 0, d = 0, k = 0, nnz = 0;
+    bool sparse = true;
+    double a2 = 0.0;
+    Math math = Math::exact;
+
+    int64_t *rp = nullptr, *trp = nullptr;
+    int32_t *ci = nullptr, *tci = nullptr;
+    double *val = nullptr, *tval = nullptr, *a_dense = nullptr;
+    double *w = nullptr, *ht = nullptr, *w_new = nullptr, *h_new = nullptr;
+    double *p = nullptr, *q = nullptr, *r = nullptr, *sm = nullptr, *norms = nullptr;
+    double *gram_scratch = nullptr, *partials = nullptr, *dot_partials = nullptr;
+    double *scalars = nullptr;  // [0] pw, [1] sq, [2..4] error report, [5] direct sum
+    double *staging = nullptr, *direct_partials = nullptr;
+    double* host_scalars = nullptr;  // pinned mirror of scalars
+    unsigned* counters = nullptr;  // K, grid-exchange arrival counters
+    double* totals = nullptr;      // K, grid-exchange published norms
+    int64_t n_partials = 0, n_direct_partials = 0;
+
+    bool s_valid = false;  // sm == gram(w) of the current w
+    uint64_t launches = 0, update_macs = 0;
+    int64_t bytes = 0;
+    int sms = 0;
+    std::vector<void*> allocs;
+
+    // cached phase-B plans, keyed by tile size
+    int64_t plan_tile = -1;
+    kern::PhaseBPlan plan_w, plan_h, plan_ref_w;
+    bool have_ref_w = false;
+
+    std::vector<cudaEvent_t> events;  // per-phase timing pool
+    long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
+    int64_t prof_n = 0;
+};
+
+namespace {
+
+using plnmf::DeviceError;
+using plnmf::guarded;
+
+template <class T>
+T* dalloc(plnmf_gpu_engine* e, int64_t n) {
+    void* ptr = nullptr;
+    const size_t bytes = sizeof(T) * (size_t)(n > 0 ? n : 1);
+    PLNMF_CUDA_CHECK(cudaMalloc(&ptr, bytes));
+    e->allocs.push_back(ptr);
+    e->bytes += (int64_t)bytes;
+    return static_cast<T*>(ptr);
+}
+
+void release(plnmf_gpu_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    if (e->s) cudaStreamSynchronize(e->s);
+    if (e->s2) cudaStreamSynchronize(e->s2);
+    for (void* ptr : e->allocs) cudaFree(ptr);
+    if (e->host_scalars) cudaFreeHost(e->host_scalars);
+    for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
+    if (e->fork) cudaEventDestroy(e->fork);
+    if (e->join) cudaEventDestroy(e->join);
+    if (e->s) cudaStreamDestroy(e->s);
+    if (e->s2) cudaStreamDestroy(e->s2);
+    delete e;
+}
+
+void check_engine(const plnmf_gpu_engine* e) {
+    if (!e) throw std::invalid_argument("plnmf_gpu: null engine");
+    PLNMF_CUDA_CHECK(cudaSetDevice(e->device));
+}
+
+void setup_common(plnmf_gpu_engine* e, int device, int64_t rank) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw DeviceError("plnmf_gpu: no CUDA device available (the engine has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("plnmf_gpu: device index out of range");
+    if (rank < 1) throw std::invalid_argument("SolverConfig: rank must be >= 1");
+    e->device = device;
+    e->k = rank;
+    PLNMF_CUDA_CHECK(cudaSetDevice(device));
+    PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
+    PLNMF_CUDA_CHECK(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+    PLNMF_CUDA_CHECK(cudaStreamCreateWithFlags(&e->s2, cudaStreamNonBlocking));
+    PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+    PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
+}
+
+void alloc_workspace(plnmf_gpu_engine* e) {
+    const int64_t v = e->v, d = e->d, k = e->k;
+    e->w = dalloc<double>(e, v * k);
+    e->w_new = dalloc<double>(e, v * k);
+    e->ht = dalloc<double>(e, d * k);
+    e->h_new = dalloc<double>(e, d * k);
+    e->p = dalloc<double>(e, v * k);
+    e->r = dalloc<double>(e, d * k);
+    e->q = dalloc<double>(e, k * k);
+    e->sm = dalloc<double>(e, k * k);
+    e->norms = dalloc<double>(e, k);
+    e->gram_scratch = dalloc<double>(e, kern::gram_scratch_doubles(std::max(v, d), k));
+    e->n_partials = k * 2 * (int64_t)e->sms;
+    e->partials = dalloc<double>(e, e->n_partials);
+    e->dot_partials = dalloc<double>(e, kern::kDotBlocks);
+    e->scalars = dalloc<double>(e, 8);
+    e->staging = dalloc<double>(e, std::max(std::max(v, d), k) * k);  // factors and K x K products
+    e->counters = dalloc<unsigned>(e, k);
+    e->totals = dalloc<double>(e, k);
+    PLNMF_CUDA_CHECK(cudaMallocHost(&e->host_scalars, sizeof(double) * 8));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->norms, 0, sizeof(double) * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->p, 0, sizeof(double) * v * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->r, 0, sizeof(double) * d * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->q, 0, sizeof(double) * k * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->sm, 0, sizeof(double) * k * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->w, 0, sizeof(double) * v * k, e->s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht, 0, sizeof(double) * d * k, e->s));
+}
+
+// ---- products ------------------------------------------------------------------------
+// R = A^T W on the main stream, S = W^T W on the side stream (skipped when the
+// last error evaluation already left gram(W) in S: same W, same deterministic
+// kernel, same bits — the reference recomputes it, proj/src/solver.cpp:34 vs
+// proj/src/hals.cpp:31).
+void precompute_h(plnmf_gpu_engine* e) {
+    const bool need_s = !e->s_valid;
+    if (need_s) {
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+        e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+    }
+    if (e->sparse)
+        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
+    else
+        e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
+    if (need_s) {
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
+        e->s_valid = true;
+    }
+}
+
+// P = A Ht (main stream), Q = Ht^T Ht (side stream).  The Gram scratch is
+// shared with S, which is never computed concurrently with Q.
+void precompute_w(plnmf_gpu_engine* e) {
+    PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+    PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
+    if (e->sparse)
+        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p);
+    else
+        e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
+    PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
+    PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
+}
+
+void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
+    if (e->plan_tile == tile) return;
+    e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device);
+    e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device);
+    if ((int64_t)e->plan_w.grid * e->k > e->n_partials)
+        throw std::logic_error("plnmf_gpu: grid-norm partial buffer too small");
+    e->plan_tile = tile;
+}
+
+// MAC counts exactly as the reference instruments them
+// (hals.cpp:70,105; tiled.cpp:49,62,152-153,172).
+uint64_t tiled_macs(int64_t n, int64_t k, int64_t tile, bool w) {
+    uint64_t m = w ? (uint64_t)n * k : 0;
+    for (int64_t b = 0; b < k; b += tile) {
+        const int64_t e = std::min(k, b + tile), width = e - b;
+        if (b > 0) m += (uint64_t)n * width * b;         // phase 1 for this tile
+        m += (uint64_t)n * width * width;                 // phase 2
+        if (w) m += 2ull * n * width;                     // normalisation
+        m += (uint64_t)n * width * (k - e);               // phase 3
+    }
+    return m;
+}
+
+void check_tile(const plnmf_config& cfg, int64_t k) {
+    if (cfg.tile_size < 1 || cfg.tile_size > k)
+        throw std::invalid_argument("iterate: tiled algorithm needs tile_size in [1, rank]");
+}
+
+long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
+    if (!std::getenv("PLNMF_PROFILE")) return nullptr;
+    if (!e->prof || e->prof_n < 8 * (int64_t)grid) {
+        e->prof_n = 8 * (int64_t)grid;
+        e->prof = dalloc<long long>(e, e->prof_n);
+    }
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->prof, 0, sizeof(long long) * e->prof_n, e->s));
+    return e->prof;
+}
+
+void prof_report(plnmf_gpu_engine* e, const char* what, int grid) {
+    std::vector<long long> h((size_t)8 * grid);
+    PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), e->prof, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, e->s));
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    const char* names[6] = {"prologue", "chain", "grid", "wait", "boundary", "lookahead"};
+    std::fprintf(stderr, "[plnmf] %s (%d CTAs) Mcycles mean/max:", what, grid);
+    for (int sct = 0; sct < 6; ++sct) {
+        double sum = 0, mx = 0;
+        for (int c = 0; c < grid; ++c) {
+            const double x = (double)h[(size_t)c * 8 + sct];
+            sum += x;
+            mx = std::max(mx, x);
+        }
+        std::fprintf(stderr, " %s %.3f/%.3f", names[sct], sum / grid / 1e6, mx / 1e6);
+    }
+    std::fprintf(stderr, "\n");
+}
+
+void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    if (alg == PLNMF_ALGORITHM_TILED) {
+        check_tile(cfg, e->k);
+        ensure_plans(e, cfg.tile_size);
+        long long* prof = prof_buffer(e, e->plan_h.grid);
+        e->launches += kern::tiled_update(e->s, e->math, e->plan_h, e->d, e->k, cfg.tile_size, cfg.epsilon, false,
+                                          e->ht, e->h_new, e->sm, e->r, nullptr, nullptr, nullptr, nullptr, prof);
+        if (prof) prof_report(e, "H update", e->plan_h.grid);
+        std::swap(e->ht, e->h_new);  // ht.swap(ws.h_new), tiled.cpp:213
+        e->update_macs += tiled_macs(e->d, e->k, cfg.tile_size, false);
+    } else {
+        e->launches += kern::reference_update_h(e->s, e->math, e->d, e->k, cfg.epsilon, e->ht, e->r, e->sm);
+        e->update_macs += (uint64_t)e->d * e->k * e->k;
+    }
+}
+
+void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    if (alg == PLNMF_ALGORITHM_TILED) {
+        check_tile(cfg, e->k);
+        ensure_plans(e, cfg.tile_size);
+        long long* prof = prof_buffer(e, e->plan_w.grid);
+        e->launches += kern::tiled_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true,
+                                          e->w, e->w_new, e->q, e->p, e->norms, e->partials, e->counters, e->totals,
+                                          prof);
+        if (prof) prof_report(e, "W update", e->plan_w.grid);
+        std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
+        e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);
+    } else {
+        if (!e->have_ref_w) {
+            e->plan_ref_w = kern::plan_reference_w(e->v, e->device);
+            if ((int64_t)e->plan_ref_w.grid * e->k > e->n_partials)
+                throw std::logic_error("plnmf_gpu: grid-norm partial buffer too small");
+            e->have_ref_w = true;
+        }
+        e->launches += kern::reference_update_w(e->s, e->math, e->plan_ref_w, e->v, e->k, cfg.epsilon, e->w, e->p,
+                                                e->q, e->norms, e->partials, e->counters, e->totals);
+        e->update_macs += (uint64_t)e->v * e->k * (e->k + 3);
+    }
+    e->s_valid = false;
+}
+
+struct ErrorReport {
+    double frob = 0, rel = 0;
+    bool cancellation = false;
+};
+
+ErrorReport direct_error(plnmf_gpu_engine* e) {
+    if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_direct: zero input matrix");
+    const int64_t np = kern::direct_residual_partials(e->v, e->d);
+    if (np > e->n_direct_partials) {
+        e->direct_partials = dalloc<double>(e, np);
+        e->n_direct_partials = np;
+    }
+    e->launches += kern::direct_residual(e->s, e->math, e->v, e->d, e->k, e->rp, e->ci, e->val, e->a_dense, e->w,
+                                         e->ht, e->direct_partials, np, e->scalars + 5);
+    PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 5, e->scalars + 5, sizeof(double), cudaMemcpyDeviceToHost, e->s));
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    ErrorReport rep;
+    rep.frob = e->host_scalars[5];
+    rep.rel = std::sqrt(rep.frob / e->a2);
+    return rep;
+}
+
+// evaluate_error, proj/src/solver.cpp:32-39
+ErrorReport evaluate_error(plnmf_gpu_engine* e) {
+    if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_gram: zero input norm");
+    e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+    e->s_valid = true;
+    e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
+    e->launches += kern::dot(e->s, e->math, e->k * e->k, e->sm, e->q, e->dot_partials, e->scalars + 1);
+    e->launches += kern::error_finalize(e->s, e->a2, e->scalars + 0, e->scalars + 1, e->scalars + 2);
+    PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 2, e->scalars + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->s));
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    ErrorReport rep;
+    rep.frob = e->host_scalars[2];
+    rep.rel = e->host_scalars[3];
+    rep.cancellation = e->host_scalars[4] != 0.0;
+    if (rep.rel < 1e-6) rep = direct_error(e);
+    return rep;
+}
+
+void upload_factor(plnmf_gpu_engine* e, const double* host_colmajor, int64_t rows, double* dst) {
+    PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->staging, host_colmajor, sizeof(double) * rows * e->k, cudaMemcpyHostToDevice, e->s));
+    e->launches += kern::colmajor_to_rowmajor(e->s, rows, e->k, e->staging, dst);
+}
+
+void download_rowmajor(plnmf_gpu_engine* e, const double* src, int64_t rows, int64_t cols, double* host_colmajor) {
+    e->launches += kern::rowmajor_to_colmajor(e->s, rows, cols, src, e->staging);
+    PLNMF_CUDA_CHECK(cudaMemcpyAsync(host_colmajor, e->staging, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, e->s));
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+}
+
+void set_factors(plnmf_gpu_engine* e, const double* w, const double* ht) {
+    if (!w || !ht) throw std::invalid_argument("set_factors: null factor");
+    upload_factor(e, w, e->v, e->w);
+    upload_factor(e, ht, e->d, e->ht);
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    e->s_valid = false;
+}
+
+void get_factors(plnmf_gpu_engine* e, double* w, double* ht) {
+    if (w) download_rowmajor(e, e->w, e->v, e->k, w);
+    if (ht) download_rowmajor(e, e->ht, e->d, e->k, ht);
+}
+
+cudaEvent_t event_at(plnmf_gpu_engine* e, size_t i) {
+    while (e->events.size() <= i) {
+        cudaEvent_t ev;
+        PLNMF_CUDA_CHECK(cudaEventCreate(&ev));
+        e->events.push_back(ev);
+    }
+    return e->events[i];
+}
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    PLNMF_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+}
+
+void add_times(plnmf_phase_times& t, const plnmf_phase_times& o) {
+    t.precompute_h += o.precompute_h; t.update_h += o.update_h; t.precompute_w += o.precompute_w;
+    t.update_w += o.update_w; t.phase1 += o.phase1; t.phase2 += o.phase2; t.phase3 += o.phase3;
+    t.normalize += o.normalize; t.error_eval += o.error_eval;
+}
+
+// iterate, proj/src/solver.cpp:53-115.  Phase buckets (PhaseTimes) come from
+// CUDA events around each step: precompute_h / precompute_w always; for the
+// reference algorithm update_h / update_w (W's normalisation is fused into
+// its kernel, so `normalize` stays 0); for the tiled algorithm the whole
+// update (init, phases 1-3, normalisation) is one fused look-ahead kernel per
+// factor and is reported in phase2 (phase1 / phase3 / normalize stay 0).
+// error_eval is host wall time of the evaluation, as in the reference.
+void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, plnmf_trace* trace) {
+    plnmf::validate_config(cfg);
+    if (cfg.rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
+    if (alg == PLNMF_ALGORITHM_TILED) check_tile(cfg, e->k);
+    if (trace && trace->records && trace->capacity < cfg.max_iters)
+        throw std::invalid_argument("iterate: trace capacity is smaller than max_iters");
+    using clock = std::chrono::steady_clock;
+    const uint64_t macs0 = e->update_macs;
+    const auto t0 = clock::now();
+    auto since = [](clock::time_point a) { return std::chrono::duration<double>(clock::now() - a).count(); };
+    plnmf_phase_times totals{};
+    const bool tiled = alg == PLNMF_ALGORITHM_TILED;
+
+    // initial error of the given factors (solver.cpp:75-76)
+    cudaEvent_t ev[8];
+    for (int i = 0; i < 8; ++i) ev[i] = event_at(e, (size_t)i);
+    PLNMF_CUDA_CHECK(cudaEventRecord(ev[0], e->s));
+    precompute_w(e);
+    PLNMF_CUDA_CHECK(cudaEventRecord(ev[1], e->s));
+    PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[1]));
+    totals.precompute_w += elapsed_s(ev[0], ev[1]);
+    auto te = clock::now();
+    const double initial = evaluate_error(e).rel;
+    totals.error_eval += since(te);
+    double prev = initial;
+    int64_t n_rec = 0;
+
+    for (int64_t it = 1; it <= cfg.max_iters; ++it) {
+        PLNMF_CUDA_CHECK(cudaEventRecord(ev[0], e->s));
+        precompute_h(e);
+        PLNMF_CUDA_CHECK(cudaEventRecord(ev[1], e->s));
+        update_h(e, cfg, alg);
+        PLNMF_CUDA_CHECK(cudaEventRecord(ev[2], e->s));
+        precompute_w(e);
+        PLNMF_CUDA_CHECK(cudaEventRecord(ev[3], e->s));
+        update_w(e, cfg, alg);
+        PLNMF_CUDA_CHECK(cudaEventRecord(ev[4], e->s));
+        PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
+        plnmf_phase_times ph{};
+        ph.precompute_h = elapsed_s(ev[0], ev[1]);
+        ph.precompute_w = elapsed_s(ev[2], ev[3]);
+        if (tiled) {
+            // one fused look-ahead kernel per update (init, phases 1-3, normalisation)
+            ph.phase2 = elapsed_s(ev[1], ev[2]) + elapsed_s(ev[3], ev[4]);
+        } else {
+            ph.update_h = elapsed_s(ev[1], ev[2]);
+            ph.update_w = elapsed_s(ev[3], ev[4]);
+        }
+        if (it % cfg.error_every == 0) {
+            te = clock::now();
+            const ErrorReport rep = evaluate_error(e);
+            ph.error_eval = since(te);
+            add_times(totals, ph);
+            if (!std::isfinite(rep.rel))
+                throw plnmf::NonFinite("iterate: objective became non-finite at iteration " + std::to_string(it));
+            if (trace && trace->records) {
+                plnmf_trace_record& rec = trace->records[n_rec];
+                rec.iteration = it;
+                rec.rel_error = rep.rel;
+                rec.elapsed_s = since(t0);
+                rec.phases = ph;
+            }
+            ++n_rec;
+            if (prev > 0.0 && std::fabs(prev - rep.rel) / prev < cfg.rel_tol) {
+                prev = rep.rel;
+                break;
+            }
+            prev = rep.rel;
+        } else {
+            add_times(totals, ph);
+        }
+    }
+    if (trace) {
+        trace->initial_error = initial;
+        trace->n_records = n_rec;
+        trace->totals = totals;
+        trace->total_seconds = since(t0);
+        trace->update_macs = e->update_macs - macs0;
+    }
+}
+
+double* product_ptr(plnmf_gpu_engine* e, plnmf_product which, int64_t& rows, int64_t& cols) {
+    switch (which) {
+        case PLNMF_PRODUCT_P: rows = e->v; cols = e->k; return e->p;
+        case PLNMF_PRODUCT_Q: rows = e->k; cols = e->k; return e->q;
+        case PLNMF_PRODUCT_R: rows = e->d; cols = e->k; return e->r;
+        case PLNMF_PRODUCT_S: rows = e->k; cols = e->k; return e->sm;
+        case PLNMF_PRODUCT_COLUMN_NORMS: rows = e->k; cols = 1; return e->norms;
+    }
+    throw std::invalid_argument("plnmf_gpu: unknown product");
+}
+
+void validate_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp, const int64_t* ci, const double* val) {
+    // CsrMatrix::validate, proj/src/csr_matrix.cpp:8-28 (same messages)
+    if (rows < 0 || cols < 0) throw std::invalid_argument("CsrMatrix: negative dimension");
+    if (!rp) throw std::invalid_argument("CsrMatrix: row_ptr length must be rows+1");
+    if (rp[0] != 0 || rp[rows] != nnz) throw std::invalid_argument("CsrMatrix: row_ptr must start at 0 and end at nnz");
+    if (nnz > 0 && (!ci || !val)) throw std::invalid_argument("CsrMatrix: col_idx and values lengths differ");
+    for (int64_t r = 0; r < rows; ++r) {
+        if (rp[r] > rp[r + 1]) throw std::invalid_argument("CsrMatrix: row_ptr must be non-decreasing");
+        for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+            if (ci[e] < 0 || ci[e] >= cols) throw std::invalid_argument("CsrMatrix: column index out of range");
+            if (e > rp[r] && ci[e] <= ci[e - 1])
+                throw std::invalid_argument("CsrMatrix: column indices must be strictly increasing per row");
+            if (!std::isfinite(val[e]) || val[e] < 0.0)
+                throw std::invalid_argument("CsrMatrix: values must be finite and non-negative");
+        }
+    }
+}
+
+}  // namespace
+
+// =============================================================================== C-ABI
+extern "C" {
+
+int32_t plnmf_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+plnmf_status plnmf_gpu_create_csr(int32_t device, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const double* values, int64_t rank,
+                                  plnmf_gpu_engine** out) {
+    plnmf_gpu_engine* e = nullptr;
+    const plnmf_status st = guarded([&] {
+        if (!out) throw std::invalid_argument("plnmf_gpu_create_csr: null output");
+        validate_csr(rows, cols, nnz, row_ptr, col_idx, values);
+        if (cols > INT32_MAX || rows > INT32_MAX)
+            throw std::invalid_argument("plnmf_gpu_create_csr: dimensions exceed int32 column indexing");
+        e = new plnmf_gpu_engine();
+        setup_common(e, device, rank);
+        e->v = rows;
+        e->d = cols;
+        e->nnz = nnz;
+        e->sparse = true;
+        double n2 = 0.0;  // InputMatrix ctor, proj/src/input_matrix.cpp:15-20 (serial)
+        for (int64_t i = 0; i < nnz; ++i) n2 += values[i] * values[i];
+        e->a2 = n2;
+        std::vector<int32_t> ci32(nnz > 0 ? nnz : 1);
+        for (int64_t i = 0; i < nnz; ++i) ci32[i] = (int32_t)col_idx[i];
+        e->rp = dalloc<int64_t>(e, rows + 1);
+        e->ci = dalloc<int32_t>(e, nnz);
+        e->val = dalloc<double>(e, nnz);
+        e->trp = dalloc<int64_t>(e, cols + 1);
+        e->tci = dalloc<int32_t>(e, nnz);
+        e->tval = dalloc<double>(e, nnz);
+        PLNMF_CUDA_CHECK(cudaMemcpy(e->rp, row_ptr, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice));
+        if (nnz > 0) {
+            PLNMF_CUDA_CHECK(cudaMemcpy(e->ci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+            PLNMF_CUDA_CHECK(cudaMemcpy(e->val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+        }
+        e->launches += kern::csr_transpose(e->s, rows, cols, nnz, e->rp, e->ci, e->val, e->trp, e->tci, e->tval);
+        alloc_workspace(e);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        *out = e;
+    });
+    if (st != PLNMF_OK) release(e);
+    return st;
+}
+
+plnmf_status plnmf_gpu_create_dense(int32_t device, int64_t rows, int64_t cols, const double* a, int64_t rank,
+                                    plnmf_gpu_engine** out) {
+    plnmf_gpu_engine* e = nullptr;
+    const plnmf_status st = guarded([&] {
+        if (!out || !a) throw std::invalid_argument("plnmf_gpu_create_dense: null argument");
+        if (rows < 0 || cols < 0) throw std::invalid_argument("DenseMatrix: negative dimension");
+        e = new plnmf_gpu_engine();
+        setup_common(e, device, rank);
+        e->v = rows;
+        e->d = cols;
+        e->sparse = false;
+        double n2 = 0.0;  // proj/src/input_matrix.cpp:5-13
+        int64_t nz = 0;
+        for (int64_t i = 0; i < rows * cols; ++i) {
+            n2 += a[i] * a[i];
+            if (a[i] != 0.0) ++nz;
+        }
+        e->a2 = n2;
+        e->nnz = nz;
+        e->a_dense = dalloc<double>(e, rows * cols);
+        double* tmp = nullptr;
+        PLNMF_CUDA_CHECK(cudaMalloc(&tmp, sizeof(double) * (size_t)std::max<int64_t>(1, rows * cols)));
+        PLNMF_CUDA_CHECK(cudaMemcpy(tmp, a, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
+        e->launches += kern::colmajor_to_rowmajor(e->s, rows, cols, tmp, e->a_dense);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        PLNMF_CUDA_CHECK(cudaFree(tmp));
+        alloc_workspace(e);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        *out = e;
+    });
+    if (st != PLNMF_OK) release(e);
+    return st;
+}
+
+plnmf_status plnmf_gpu_destroy(plnmf_gpu_engine* e) {
+    return guarded([&] { release(e); });
+}
+
+plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int64_t* cols, int64_t* nnz, double* norm_sq) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("plnmf_gpu: null engine");
+        if (rows) *rows = e->v;
+        if (cols) *cols = e->d;
+        if (nnz) *nnz = e->nnz;
+        if (norm_sq) *norm_sq = e->a2;
+    });
+}
+
+plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
+    return guarded([&] {
+        check_engine(e);
+        if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED) throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
+        e->math = math == PLNMF_MATH_EXACT ? Math::exact : Math::fused;
+        e->s_valid = false;
+    });
+}
+
+plnmf_status plnmf_gpu_set_factors(plnmf_gpu_engine* e, const double* w, const double* ht) {
+    return guarded([&] { check_engine(e); set_factors(e, w, ht); });
+}
+
+plnmf_status plnmf_gpu_get_factors(plnmf_gpu_engine* e, double* w, double* ht) {
+    return guarded([&] { check_engine(e); get_factors(e, w, ht); });
+}
+
+plnmf_status plnmf_gpu_init_factors(plnmf_gpu_engine* e, const plnmf_config* cfg) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_init_factors: null config");
+        if (cfg->rank != e->k) throw std::invalid_argument("init_factors: rank does not match the engine");
+        std::vector<double> w((size_t)(e->v * e->k)), ht((size_t)(e->d * e->k));
+        plnmf::init_factors_host(e->v, e->d, *cfg, w.data(), ht.data());
+        set_factors(e, w.data(), ht.data());
+    });
+}
+
+plnmf_status plnmf_gpu_iterate(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg, plnmf_trace* trace) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_iterate: null config");
+        iterate(e, *cfg, alg, trace);
+    });
+}
+
+plnmf_status plnmf_gpu_iterate_host(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg, double* w,
+                                    double* ht, plnmf_trace* trace) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_iterate_host: null config");
+        set_factors(e, w, ht);
+        iterate(e, *cfg, alg, trace);
+        get_factors(e, w, ht);
+    });
+}
+
+plnmf_status plnmf_gpu_precompute_h_products(plnmf_gpu_engine* e) {
+    return guarded([&] { check_engine(e); precompute_h(e); PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s)); });
+}
+
+plnmf_status plnmf_gpu_precompute_w_products(plnmf_gpu_engine* e) {
+    return guarded([&] { check_engine(e); precompute_w(e); PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s)); });
+}
+
+plnmf_status plnmf_gpu_update_h(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_update_h: null config");
+        update_h(e, *cfg, alg);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    });
+}
+
+plnmf_status plnmf_gpu_update_w(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_update_w: null config");
+        update_w(e, *cfg, alg);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    });
+}
+
+plnmf_status plnmf_gpu_evaluate_error(plnmf_gpu_engine* e, double* out3) {
+    return guarded([&] {
+        check_engine(e);
+        const ErrorReport r = evaluate_error(e);
+        if (out3) {
+            out3[0] = r.frob;
+            out3[1] = r.rel;
+            out3[2] = r.cancellation ? 1.0 : 0.0;
+        }
+    });
+}
+
+plnmf_status plnmf_gpu_relative_error_direct(plnmf_gpu_engine* e, double* out2) {
+    return guarded([&] {
+        check_engine(e);
+        const ErrorReport r = direct_error(e);
+        if (out2) {
+            out2[0] = r.frob;
+            out2[1] = r.rel;
+        }
+    });
+}
+
+plnmf_status plnmf_gpu_get_product(plnmf_gpu_engine* e, plnmf_product which, double* out) {
+    return guarded([&] {
+        check_engine(e);
+        if (!out) throw std::invalid_argument("plnmf_gpu_get_product: null output");
+        int64_t rows, cols;
+        double* src = product_ptr(e, which, rows, cols);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        if (cols == 1) {
+            PLNMF_CUDA_CHECK(cudaMemcpy(out, src, sizeof(double) * rows, cudaMemcpyDeviceToHost));
+        } else {
+            download_rowmajor(e, src, rows, cols, out);
+        }
+    });
+}
+
+plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which, const double* in) {
+    return guarded([&] {
+        check_engine(e);
+        if (!in) throw std::invalid_argument("plnmf_gpu_set_product: null input");
+        int64_t rows, cols;
+        double* dst = product_ptr(e, which, rows, cols);
+        if (cols == 1) {
+            PLNMF_CUDA_CHECK(cudaMemcpy(dst, in, sizeof(double) * rows, cudaMemcpyHostToDevice));
+        } else {
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->staging, in, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, e->s));
+            e->launches += kern::colmajor_to_rowmajor(e->s, rows, cols, e->staging, dst);
+            PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        }
+        if (which == PLNMF_PRODUCT_S) e->s_valid = false;
+    });
+}
+
+plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg, int64_t n,
+                                      double* device_ms) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg) throw std::invalid_argument("plnmf_gpu_run_iterations: null config");
+        plnmf::validate_config(*cfg);
+        if (cfg->rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
+        cudaEvent_t a = event_at(e, 0), b = event_at(e, 1);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        PLNMF_CUDA_CHECK(cudaEventRecord(a, e->s));
+        for (int64_t i = 0; i < n; ++i) {
+            precompute_h(e);
+            update_h(e, *cfg, alg);
+            precompute_w(e);
+            update_w(e, *cfg, alg);
+        }
+        PLNMF_CUDA_CHECK(cudaEventRecord(b, e->s));
+        PLNMF_CUDA_CHECK(cudaEventSynchronize(b));
+        if (device_ms) *device_ms = elapsed_s(a, b) * 1e3;
+    });
+}
+
+plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg, int32_t which, int32_t reps,
+                                   double* avg_ms) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg || reps < 1) throw std::invalid_argument("plnmf_gpu_time_kernel: bad argument");
+        cudaEvent_t a = event_at(e, 0), b = event_at(e, 1);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
+        auto once = [&] {
+            switch (which) {
+                case 0:
+                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p);
+                    else e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
+                    break;
+                case 1:
+                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
+                    else e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
+                    break;
+                case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch); break;
+                case 3:  // successive W updates against the same P, Q (mutates W)
+                    update_w(e, *cfg, cfg->tile_size > 0 ? PLNMF_ALGORITHM_TILED : PLNMF_ALGORITHM_REFERENCE);
+                    break;
+                case 4: update_h(e, *cfg, cfg->tile_size > 0 ? PLNMF_ALGORITHM_TILED : PLNMF_ALGORITHM_REFERENCE); break;
+                default: throw std::invalid_argument("plnmf_gpu_time_kernel: unknown kernel family");
+            }
+        };
+        once();  // warm
+        PLNMF_CUDA_CHECK(cudaEventRecord(a, e->s));
+        for (int i = 0; i < reps; ++i) once();
+        PLNMF_CUDA_CHECK(cudaEventRecord(b, e->s));
+        PLNMF_CUDA_CHECK(cudaEventSynchronize(b));
+        if (avg_ms) *avg_ms = elapsed_s(a, b) * 1e3 / reps;
+        e->s_valid = false;
+    });
+}
+
+plnmf_status plnmf_gpu_get_stats(const plnmf_gpu_engine* e, plnmf_gpu_stats* out) {
+    return guarded([&] {
+        if (!e || !out) throw std::invalid_argument("plnmf_gpu_get_stats: null argument");
+        out->kernel_launches = e->launches;
+        out->persistent_ctas = e->plan_w.grid;
+        out->sm_count = e->sms;
+        out->device_bytes = e->bytes;
+    });
+}
+
+plnmf_status plnmf_gpu_synchronize(plnmf_gpu_engine* e) {
+    return guarded([&] {
+        check_engine(e);
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,282 @@
+// K3 Gram products S = W^T W, Q = Ht^T Ht, and K8 dense-A products.
+//
+// gram: replaces gram_into (proj/src/linalg.cpp:168-204).  The reference sums
+// each upper-triangle entry over 2048-row blocks; inside a block its
+// `omp simd reduction` runs as two SSE2 lanes (even / odd row offsets, an odd
+// tail row into lane 0, combined as (lane0 + 0.0) + lane1 — objdump of the
+// Release linalg.o), and the blocks are added to g in order.  Here one CTA
+// computes a 32x32 tile of entries for one 2048-row block, each thread a 4x4
+// register tile with separate even/odd accumulators, rows streamed through
+// shared memory in ascending order — the same per-entry operation sequence.
+// A second kernel adds the per-block partials in block order and mirrors.
+//
+// dense_a_ht / dense_at_w: replace gemm(..., a.dense(), ...) at
+// proj/src/hals.cpp:29,43 (accumulate_nn / accumulate_tn, linalg.cpp:45-79)
+// with register-tiled SIMT GEMMs in the same per-element order
+// (P: ascending inner index; R: two lanes over all V rows).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace plnmf {
+namespace {
+
+constexpr int kGramTile = 32;
+constexpr int kGramRows = 64;  // rows staged per shared-memory chunk (even)
+constexpr int kGramBlock = 2048;  // proj/src/linalg.cpp:188 kRowBlock
+constexpr int kGramThreads = 64;  // 8 x 8 threads, 4 x 4 entries each
+
+__device__ __forceinline__ void decode_upper(int p, int ntile, int& ta, int& tb) {
+    ta = 0;
+    int row_len = ntile;
+    while (p >= row_len) {
+        p -= row_len;
+        ++ta;
+        --row_len;
+    }
+    tb = ta + p;
+}
+
+template <class M>
+__global__ void __launch_bounds__(kGramThreads) gram_block_kernel(int64_t n, int k,
+                                                                  const double* __restrict__ m,
+                                                                  double* __restrict__ part,
+                                                                  int ntile) {
+    __shared__ double As[kGramRows][kGramTile];
+    __shared__ double Bs[kGramRows][kGramTile];
+    int ta, tb;
+    decode_upper(blockIdx.x, ntile, ta, tb);
+    const int64_t blk = blockIdx.y;
+    const int64_t v0 = blk * kGramBlock;
+    const int64_t v1 = (v0 + kGramBlock < n) ? v0 + kGramBlock : n;
+    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+    const int a0 = ta * kGramTile, b0 = tb * kGramTile;
+
+    double e[4][4], o[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[i][j] = o[i][j] = 0.0;
+
+    for (int64_t r0 = v0; r0 < v1; r0 += kGramRows) {
+        const int nr = (int)((v1 - r0) < kGramRows ? (v1 - r0) : kGramRows);
+        for (int idx = threadIdx.x; idx < kGramRows * kGramTile; idx += kGramThreads) {
+            const int rr = idx / kGramTile, cc = idx % kGramTile;
+            const bool rok = rr < nr;
+            As[rr][cc] = (rok && a0 + cc < k) ? m[(r0 + rr) * k + a0 + cc] : 0.0;
+            Bs[rr][cc] = (rok && b0 + cc < k) ? m[(r0 + rr) * k + b0 + cc] : 0.0;
+        }
+        __syncthreads();
+        // r0 - v0 is a multiple of kGramRows (even): offset parity == rr parity.
+        for (int rr = 0; rr < nr; rr += 2) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[rr][ty + 8 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[rr][tx + 8 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) e[i][j] = M::madd(e[i][j], av[i], bv[j]);
+            if (rr + 1 < nr) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[i] = As[rr + 1][ty + 8 * i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bv[j] = Bs[rr + 1][tx + 8 * j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) o[i][j] = M::madd(o[i][j], av[i], bv[j]);
+            }
+        }
+        __syncthreads();
+    }
+    double* pb = part + blk * (int64_t)k * k;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int a = a0 + ty + 8 * i, b = b0 + tx + 8 * j;
+            if (a < k && b < k) pb[(int64_t)a * k + b] = dadd(dadd(e[i][j], 0.0), o[i][j]);
+        }
+}
+
+// g(a,b) = g(b,a) = sum over blocks in order (g starts at 0, g += acc).
+__global__ void gram_combine_kernel(int k, int64_t nblk, const double* __restrict__ part,
+                                    double* __restrict__ g) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)k * k) return;
+    const int a = (int)(idx / k), b = (int)(idx % k);
+    if (a > b) return;
+    double s = 0.0;
+    for (int64_t blk = 0; blk < nblk; ++blk) s = dadd(s, part[(blk * k + a) * k + b]);
+    g[(int64_t)a * k + b] = s;
+    g[(int64_t)b * k + a] = s;
+}
+
+// ---- dense-A products --------------------------------------------------------------
+constexpr int kGemmTile = 64;
+constexpr int kGemmK = 16;
+constexpr int kGemmThreads = 256;  // 16 x 16, 4 x 4 outputs each
+
+// p(v, j) = sum_{kk ascending} ht(kk, j) * a(v, kk), from 0 (accumulate_nn with
+// alpha = 1: f = alpha*b(kk,j), c += f * a(i,kk)).
+template <class M>
+__global__ void __launch_bounds__(kGemmThreads) dense_a_ht_kernel(int64_t v, int64_t d, int k,
+                                                                  const double* __restrict__ a,
+                                                                  const double* __restrict__ ht,
+                                                                  double* __restrict__ p) {
+    __shared__ double As[kGemmK][kGemmTile + 1];
+    __shared__ double Bs[kGemmK][kGemmTile];
+    const int64_t r0 = (int64_t)blockIdx.y * kGemmTile;
+    const int c0 = blockIdx.x * kGemmTile;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int64_t k0 = 0; k0 < d; k0 += kGemmK) {
+        for (int idx = threadIdx.x; idx < kGemmK * kGemmTile; idx += kGemmThreads) {
+            const int rr = idx / kGemmK, kk = idx % kGemmK;
+            As[kk][rr] = (r0 + rr < v && k0 + kk < d) ? a[(r0 + rr) * d + k0 + kk] : 0.0;
+            const int kb = idx / kGemmTile, cc = idx % kGemmTile;
+            Bs[kb][cc] = (k0 + kb < d && c0 + cc < k) ? 1.0 * ht[(k0 + kb) * k + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (int)((d - k0) < kGemmK ? (d - k0) : kGemmK);
+        for (int kk = 0; kk < kmax; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = M::madd(acc[i][j], bv[j], av[i]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t r = r0 + ty + 16 * i;
+            const int c = c0 + tx + 16 * j;
+            if (r < v && c < k) p[r * k + c] = acc[i][j];
+        }
+}
+
+// r(dd, j) = 0 + 1.0 * ((lane0 + 0.0) + lane1), lanes = even / odd v over all
+// V rows (accumulate_tn's simd reduction, linalg.cpp:71-75, after the beta=0
+// zero fill at :31-42).
+template <class M>
+__global__ void __launch_bounds__(kGemmThreads) dense_at_w_kernel(int64_t v, int64_t d, int k,
+                                                                  const double* __restrict__ a,
+                                                                  const double* __restrict__ w,
+                                                                  double* __restrict__ r) {
+    __shared__ double As[kGemmK][kGemmTile];
+    __shared__ double Bs[kGemmK][kGemmTile];
+    const int64_t r0 = (int64_t)blockIdx.y * kGemmTile;  // output rows = columns of A
+    const int c0 = blockIdx.x * kGemmTile;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double e[4][4], o[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[i][j] = o[i][j] = 0.0;
+    for (int64_t v0 = 0; v0 < v; v0 += kGemmK) {  // kGemmK even: parity of kk == parity of row
+        for (int idx = threadIdx.x; idx < kGemmK * kGemmTile; idx += kGemmThreads) {
+            const int kk = idx / kGemmTile, cc = idx % kGemmTile;
+            As[kk][cc] = (v0 + kk < v && r0 + cc < d) ? a[(v0 + kk) * d + r0 + cc] : 0.0;
+            Bs[kk][cc] = (v0 + kk < v && c0 + cc < k) ? w[(v0 + kk) * k + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (int)((v - v0) < kGemmK ? (v - v0) : kGemmK);
+        for (int kk = 0; kk < kmax; kk += 2) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) e[i][j] = M::madd(e[i][j], av[i], bv[j]);
+            if (kk + 1 < kmax) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[i] = As[kk + 1][ty + 16 * i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bv[j] = Bs[kk + 1][tx + 16 * j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) o[i][j] = M::madd(o[i][j], av[i], bv[j]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t rr = r0 + ty + 16 * i;
+            const int c = c0 + tx + 16 * j;
+            if (rr < d && c < k) r[rr * k + c] = dadd(0.0, dmul(1.0, dadd(dadd(e[i][j], 0.0), o[i][j])));
+        }
+}
+
+}  // namespace
+
+namespace kern {
+
+int64_t gram_scratch_doubles(int64_t n, int64_t k) {
+    const int64_t nblk = (n + kGramBlock - 1) / kGramBlock;
+    return (nblk > 0 ? nblk : 1) * k * k;
+}
+
+int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double* g,
+         double* scratch) {
+    if (k <= 0) return 0;
+    const int64_t nblk = (n + kGramBlock - 1) / kGramBlock;
+    if (nblk == 0) {
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(g, 0, sizeof(double) * k * k, s));
+        return 0;
+    }
+    const int ntile = (int)((k + kGramTile - 1) / kGramTile);
+    const dim3 grid((unsigned)(ntile * (ntile + 1) / 2), (unsigned)nblk);
+    if (m == Math::exact)
+        gram_block_kernel<MathExact><<<grid, kGramThreads, 0, s>>>(n, (int)k, mat, scratch, ntile);
+    else
+        gram_block_kernel<MathFused><<<grid, kGramThreads, 0, s>>>(n, (int)k, mat, scratch, ntile);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    const int64_t tot = k * k;
+    gram_combine_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((int)k, nblk, scratch, g);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return 2;
+}
+
+int dense_a_ht(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const double* a,
+               const double* ht, double* p) {
+    const dim3 grid((unsigned)((k + kGemmTile - 1) / kGemmTile), (unsigned)((v + kGemmTile - 1) / kGemmTile));
+    if (m == Math::exact)
+        dense_a_ht_kernel<MathExact><<<grid, kGemmThreads, 0, s>>>(v, d, (int)k, a, ht, p);
+    else
+        dense_a_ht_kernel<MathFused><<<grid, kGemmThreads, 0, s>>>(v, d, (int)k, a, ht, p);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return 1;
+}
+
+int dense_at_w(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const double* a,
+               const double* w, double* r) {
+    const dim3 grid((unsigned)((k + kGemmTile - 1) / kGemmTile), (unsigned)((d + kGemmTile - 1) / kGemmTile));
+    if (m == Math::exact)
+        dense_at_w_kernel<MathExact><<<grid, kGemmThreads, 0, s>>>(v, d, (int)k, a, w, r);
+    else
+        dense_at_w_kernel<MathFused><<<grid, kGemmThreads, 0, s>>>(v, d, (int)k, a, w, r);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return 1;
+}
+
+}  // namespace kern
+}  // namespace plnmf

@@ -1,0 +1,99 @@
+// Launchers of the engine's sm_100a kernels.  Device layout: every dense
+// matrix is ROW-major fp64 (row r contiguous, leading dimension = #cols);
+// sparse matrices are CSR with int64 row pointers and int32 column indices.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "host.hpp"
+
+namespace plnmf {
+
+struct CudaError : DeviceError {
+    cudaError_t code;
+    CudaError(cudaError_t c, const char* expr, const char* file, int line)
+        : DeviceError(std::string("CUDA error ") + cudaGetErrorString(c) + " at " + file + ":" +
+                      std::to_string(line) + " (" + expr + ")"),
+          code(c) {}
+};
+
+enum class Math : int { exact = 0, fused = 1 };
+
+// Every launcher returns the number of kernels it launched (for the
+// engine's launch counter).
+namespace kern {
+
+// y := a * x over CSR a (rows x ?), x row-major (? x k), y row-major (rows x k).
+// Per element: acc = 0; acc += val[e] * x[col[e]][j] for e ascending —
+// proj/src/linalg.cpp:139-154.
+int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
+             const double* val, const double* x, int64_t k, double* y);
+
+// g := m^T m (k x k) for row-major m (n x k), in the reference's compiled
+// order (2048-row blocks, even/odd lanes, proj/src/linalg.cpp:168-204).
+// scratch: gram_scratch_doubles(n, k) doubles.
+int64_t gram_scratch_doubles(int64_t n, int64_t k);
+int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double* g,
+         double* scratch);
+
+// Dense products for a dense input A (row-major v x d on the device).
+// p := A * ht    (proj/src/hals.cpp:43 -> accumulate_nn, linalg.cpp:45-59)
+int dense_a_ht(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const double* a,
+               const double* ht, double* p);
+// r := A^T * w   (proj/src/hals.cpp:29 -> accumulate_tn, linalg.cpp:62-79)
+int dense_at_w(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const double* a,
+               const double* w, double* r);
+
+// ---- tiled (PL-NMF) update, proj/src/tiled.cpp:176-214 --------------------------
+struct PhaseBPlan {
+    int grid = 0;            // CTAs
+    int64_t rows_per_cta = 0;
+    size_t smem = 0;         // dynamic shared memory bytes
+    bool cooperative = false;
+};
+// One look-ahead kernel per update: init_new_accumulator (:28-50), phase 1
+// (:52-65), and per tile phase 2 (:67-156) + phase 3 (:158-174).  w_update =>
+// init scales by the diagonal and every column is L2-normalised with a
+// grid-wide exchange (cooperative persistent launch, one CTA per SM).
+PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
+int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
+                 double eps, bool w_update, const double* old_m, double* out, const double* coeff,
+                 const double* add, double* norms, double* partials, unsigned* counters, double* totals,
+                 long long* prof = nullptr);
+
+// ---- reference (fast-hals) updaters, proj/src/hals.cpp --------------------------
+int reference_update_h(cudaStream_t s, Math m, int64_t d, int64_t k, double eps, double* ht,
+                       const double* r, const double* sm);
+PhaseBPlan plan_reference_w(int64_t v, int device);
+int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v, int64_t k,
+                       double eps, double* w, const double* p, const double* q, double* norms,
+                       double* partials, unsigned* counters, double* totals);
+
+// ---- metrics ---------------------------------------------------------------------
+// out := sum_i a[i]*b[i] (n elements), fixed-order two-pass reduction.
+constexpr int kDotBlocks = 296;
+int dot(cudaStream_t s, Math m, int64_t n, const double* a, const double* b, double* partials,
+        double* out);
+// out3 := {frob_sq, relative, cancellation} from a2, *pw, *sq (metrics.cpp:115-126)
+int error_finalize(cudaStream_t s, double a2, const double* pw, const double* sq, double* out3);
+// Direct residual ||A - W Ht^T||_F^2 for CSR A (metrics.cpp:49-75) or dense A.
+int direct_residual(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const int64_t* rp,
+                    const int32_t* ci, const double* val, const double* a_dense, const double* w,
+                    const double* ht, double* partials, int64_t n_partials, double* out);
+int64_t direct_residual_partials(int64_t v, int64_t d);
+
+// ---- layout / structure ------------------------------------------------------------
+// dst (rows x cols, row-major) := src (rows x cols, column-major), and back.
+int colmajor_to_rowmajor(cudaStream_t s, int64_t rows, int64_t cols, const double* src, double* dst);
+int rowmajor_to_colmajor(cudaStream_t s, int64_t rows, int64_t cols, const double* src, double* dst);
+// CSR (rows x cols) -> CSR of the transpose, entries of each output row in
+// ascending source-row order (proj/src/csr_matrix.cpp:30-50).
+int csr_transpose(cudaStream_t s, int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp,
+                  const int32_t* ci, const double* val, int64_t* trp, int32_t* tci, double* tval);
+
+}  // namespace kern
+}  // namespace plnmf

@@ -1,0 +1,131 @@
+// K1/K2 — CSR SpMM y := a * x on sm_100a.
+//
+// Replaces spmm_into (proj/src/linalg.cpp:139-154), called as A*Ht
+// (proj/src/hals.cpp:41) and as A^T*W on the cached transpose (hals.cpp:26-27).
+//
+// One warp per sparse row.  The dense operand is row-major, so each nonzero
+// gathers one contiguous K-wide factor row: lane l owns columns l, l+32, ...,
+// and a gather is NC coalesced 256-byte warp loads.  The row's (col, val)
+// pairs are loaded 32 at a time, coalesced, and broadcast by shuffle.  Each
+// output element accumulates its terms in ascending nonzero order starting
+// from 0.0 — the reference's order — so with Math::exact the result is
+// bit-identical to spmm_into.  Gathers of UNROLL nonzeros are issued before
+// their adds to keep NC*UNROLL independent loads in flight per lane.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace plnmf {
+namespace {
+
+constexpr int kSpmmThreads = 256;
+constexpr int kUnroll = 4;
+
+template <int NC, class M>
+__global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(
+    int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+    const double* __restrict__ val, const double* __restrict__ x, int64_t ldx,
+    double* __restrict__ y, int64_t ldy, int col0, int ncols) {
+    const int64_t row = (int64_t)blockIdx.x * (kSpmmThreads / kWarp) + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int lane = lane_id();
+    const int64_t e0 = rp[row], e1 = rp[row + 1];
+
+    double acc[NC];
+    bool ok[NC];
+#pragma unroll
+    for (int g = 0; g < NC; ++g) {
+        acc[g] = 0.0;
+        ok[g] = lane + kWarp * g < ncols;
+    }
+    const double* xb = x + col0 + lane;
+
+    for (int64_t base = e0; base < e1; base += kWarp) {
+        const int cnt = (int)((e1 - base) < kWarp ? (e1 - base) : kWarp);
+        int c = 0;
+        double a = 0.0;
+        if (lane < cnt) {
+            c = __ldg(ci + base + lane);
+            a = __ldg(val + base + lane);
+        }
+        int i = 0;
+        for (; i + kUnroll <= cnt; i += kUnroll) {
+            double xv[kUnroll][NC];
+            double av[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int cc = __shfl_sync(0xffffffffu, c, i + u);
+                av[u] = __shfl_sync(0xffffffffu, a, i + u);
+                const double* xr = xb + (int64_t)cc * ldx;
+#pragma unroll
+                for (int g = 0; g < NC; ++g) xv[u][g] = ok[g] ? __ldg(xr + kWarp * g) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int g = 0; g < NC; ++g) acc[g] = M::madd(acc[g], av[u], xv[u][g]);
+        }
+        for (; i < cnt; ++i) {
+            const int cc = __shfl_sync(0xffffffffu, c, i);
+            const double aa = __shfl_sync(0xffffffffu, a, i);
+            const double* xr = xb + (int64_t)cc * ldx;
+#pragma unroll
+            for (int g = 0; g < NC; ++g)
+                acc[g] = M::madd(acc[g], aa, ok[g] ? __ldg(xr + kWarp * g) : 0.0);
+        }
+    }
+    double* yr = y + row * ldy + col0 + lane;
+#pragma unroll
+    for (int g = 0; g < NC; ++g)
+        if (ok[g]) yr[kWarp * g] = acc[g];
+}
+
+template <class M>
+void launch_pass(cudaStream_t s, int nc, int64_t rows, const int64_t* rp, const int32_t* ci,
+                 const double* val, const double* x, int64_t k, double* y, int col0, int ncols) {
+    const dim3 grid((unsigned)((rows + kSpmmThreads / kWarp - 1) / (kSpmmThreads / kWarp)));
+#define PLNMF_SPMM_CASE(N)                                                                   \
+    case N:                                                                                  \
+        spmm_csr_kernel<N, M><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k,   \
+                                                            col0, ncols);                    \
+        break;
+    switch (nc) {
+        PLNMF_SPMM_CASE(1)
+        PLNMF_SPMM_CASE(2)
+        PLNMF_SPMM_CASE(3)
+        PLNMF_SPMM_CASE(4)
+        PLNMF_SPMM_CASE(5)
+        PLNMF_SPMM_CASE(6)
+        PLNMF_SPMM_CASE(7)
+        PLNMF_SPMM_CASE(8)
+        default: throw std::logic_error("spmm: bad column-group count");
+    }
+#undef PLNMF_SPMM_CASE
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace
+
+namespace kern {
+
+int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
+             const double* val, const double* x, int64_t k, double* y) {
+    if (rows <= 0 || k <= 0) return 0;
+    // Columns are processed in passes of at most 256 (8 warp-wide groups);
+    // passes split K evenly so no pass is nearly empty.
+    const int64_t passes = (k + 255) / 256;
+    const int64_t per = (k + passes - 1) / passes;
+    int launches = 0;
+    for (int64_t c0 = 0; c0 < k; c0 += per) {
+        const int ncols = (int)((k - c0) < per ? (k - c0) : per);
+        const int nc = (ncols + kWarp - 1) / kWarp;
+        if (m == Math::exact)
+            launch_pass<MathExact>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols);
+        else
+            launch_pass<MathFused>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols);
+        ++launches;
+    }
+    return launches;
+}
+
+}  // namespace kern
+}  // namespace plnmf

@@ -1,0 +1,152 @@
+// Microbenchmark of grid-wide deterministic sum exchanges (one CTA per SM),
+// the per-column critical step of the W update.  Build + run:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/xb tools/exchange_bench.cu && /tmp/xb
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ double ldr(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void str(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ldru(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double wsum(double v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(~0u, v, o);
+    return v;
+}
+
+constexpr int MAXL = 8;
+
+// variant 0: acq_rel atomic, last arriver sums, publish, poll total
+// variant 1: relaxed atomic + NaN-sentinel partials (no fences), last sums, poll total
+// variant 2: all CTAs poll all NaN-sentinel partials (with backoff)
+// variant 3: relaxed red arrival; lane 0 polls counter; then all read partials (NaN-guarded)
+template <int VAR>
+__global__ void xkernel(int ncol, double* partials, unsigned* counters, double* totals, double* out, int sleep_ns) {
+    const int g = gridDim.x, lane = threadIdx.x & 31;
+    double acc = 0;
+    for (int t = 0; t < ncol; ++t) {
+        const double blk = 1.0 + blockIdx.x + t;
+        if (threadIdx.x < 32) {
+            double* col = partials + (size_t)t * g;
+            double norm = 0;
+            if (VAR == 0 || VAR == 1) {
+                unsigned prev = 0;
+                if (lane == 0) {
+                    str(col + blockIdx.x, blk);
+                    if (VAR == 0)
+                        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counters + t) : "memory");
+                    else
+                        asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counters + t) : "memory");
+                }
+                prev = __shfl_sync(~0u, prev, 0);
+                if (prev == (unsigned)g - 1) {
+                    double v[MAXL];
+                    for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? ldr(col + lane + 32 * i) : 0.0;
+                    for (;;) {
+                        bool pend = false;
+                        for (int i = 0; i < MAXL; ++i) pend |= isnan(v[i]);
+                        if (!__any_sync(~0u, pend)) break;
+                        for (int i = 0; i < MAXL; ++i)
+                            if (isnan(v[i])) v[i] = ldr(col + lane + 32 * i);
+                    }
+                    double s = 0;
+                    for (int i = 0; i < MAXL; ++i) s += v[i];
+                    s = wsum(s);
+                    if (lane == 0) str(totals + t, s);
+                }
+                if (lane == 0) {
+                    norm = ldr(totals + t);
+                    while (isnan(norm)) {
+                        if (sleep_ns) __nanosleep(sleep_ns);
+                        norm = ldr(totals + t);
+                    }
+                }
+                norm = __shfl_sync(~0u, norm, 0);
+            } else if (VAR == 2) {
+                if (lane == 0) str(col + blockIdx.x, blk);
+                double v[MAXL];
+                for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? ldr(col + lane + 32 * i) : 0.0;
+                for (;;) {
+                    bool pend = false;
+                    for (int i = 0; i < MAXL; ++i) pend |= isnan(v[i]);
+                    if (!__any_sync(~0u, pend)) break;
+                    if (sleep_ns) __nanosleep(sleep_ns);
+                    for (int i = 0; i < MAXL; ++i)
+                        if (isnan(v[i])) v[i] = ldr(col + lane + 32 * i);
+                }
+                double s = 0;
+                for (int i = 0; i < MAXL; ++i) s += v[i];
+                norm = __shfl_sync(~0u, wsum(s), 0);
+            } else {
+                if (lane == 0) {
+                    str(col + blockIdx.x, blk);
+                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(counters + t) : "memory");
+                    while (ldru(counters + t) < (unsigned)g)
+                        if (sleep_ns) __nanosleep(sleep_ns);
+                }
+                __syncwarp();
+                double v[MAXL];
+                for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? ldr(col + lane + 32 * i) : 0.0;
+                for (;;) {
+                    bool pend = false;
+                    for (int i = 0; i < MAXL; ++i) pend |= isnan(v[i]);
+                    if (!__any_sync(~0u, pend)) break;
+                    for (int i = 0; i < MAXL; ++i)
+                        if (isnan(v[i])) v[i] = ldr(col + lane + 32 * i);
+                }
+                double s = 0;
+                for (int i = 0; i < MAXL; ++i) s += v[i];
+                norm = __shfl_sync(~0u, wsum(s), 0);
+            }
+            acc += norm;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int ncol = 240, g = sms;
+    double *partials, *totals, *out;
+    unsigned* counters;
+    cudaMalloc(&partials, sizeof(double) * ncol * g);
+    cudaMalloc(&totals, sizeof(double) * ncol);
+    cudaMalloc(&out, sizeof(double) * g);
+    cudaMalloc(&counters, sizeof(unsigned) * ncol);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const char* names[4] = {"acq_rel atomic + last sums", "relaxed atomic + NaN partials", "all poll all partials",
+                            "red arrive + counter poll + read"};
+    for (int var = 0; var < 4; ++var)
+        for (int sl : {0, 16, 64}) {
+            float best = 1e9;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaMemset(partials, 0xFF, sizeof(double) * ncol * g);
+                cudaMemset(totals, 0xFF, sizeof(double) * ncol);
+                cudaMemset(counters, 0, sizeof(unsigned) * ncol);
+                cudaEventRecord(a);
+                void* args[] = {(void*)&ncol, &partials, &counters, &totals, &out, &sl};
+                void* fn = var == 0 ? (void*)xkernel<0> : var == 1 ? (void*)xkernel<1> : var == 2 ? (void*)xkernel<2> : (void*)xkernel<3>;
+                cudaLaunchCooperativeKernel(fn, g, 512, args, 0, 0);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                if (ms < best) best = ms;
+            }
+            printf("%-36s sleep=%3d ns: %7.3f us per exchange (%s)\n", names[var], sl, best * 1e3 / ncol,
+                   cudaGetErrorString(cudaGetLastError()));
+        }
+    return 0;
+}
