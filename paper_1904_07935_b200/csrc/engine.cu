@@ -125,12 +125,12 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     e->sm = dalloc<double>(e, k * k);
     e->norms = dalloc<double>(e, k);
     e->gram_scratch = dalloc<double>(e, kern::gram_scratch_doubles(std::max(v, d), k));
-    e->n_partials = k * 2 * (int64_t)e->sms;
+    e->n_partials = kern::exchange_partials_doubles(k, 2 * e->sms);
     e->partials = dalloc<double>(e, e->n_partials);
     e->dot_partials = dalloc<double>(e, kern::kDotBlocks);
     e->scalars = dalloc<double>(e, 8);
     e->staging = dalloc<double>(e, std::max(std::max(v, d), k) * k);  // factors and K x K products
-    e->counters = dalloc<unsigned>(e, k);
+    e->counters = dalloc<unsigned>(e, kern::exchange_counters(k));
     e->totals = dalloc<double>(e, k);
     PLNMF_CUDA_CHECK(cudaMallocHost(&e->host_scalars, sizeof(double) * 8));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->norms, 0, sizeof(double) * k, e->s));
@@ -183,7 +183,7 @@ void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
     if (e->plan_tile == tile) return;
     e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device);
     e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device);
-    if ((int64_t)e->plan_w.grid * e->k > e->n_partials)
+    if (kern::exchange_partials_doubles(e->k, e->plan_w.grid) > e->n_partials)
         throw std::logic_error("plnmf_gpu: grid-norm partial buffer too small");
     e->plan_tile = tile;
 }
@@ -209,8 +209,8 @@ void check_tile(const plnmf_config& cfg, int64_t k) {
 
 long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
     if (!std::getenv("PLNMF_PROFILE")) return nullptr;
-    if (!e->prof || e->prof_n < 8 * (int64_t)grid) {
-        e->prof_n = 8 * (int64_t)grid;
+    if (!e->prof || e->prof_n < 16 * (int64_t)grid) {
+        e->prof_n = 16 * (int64_t)grid;
         e->prof = dalloc<long long>(e, e->prof_n);
     }
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->prof, 0, sizeof(long long) * e->prof_n, e->s));
@@ -218,21 +218,24 @@ long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
 }
 
 void prof_report(plnmf_gpu_engine* e, const char* what, int grid) {
-    std::vector<long long> h((size_t)8 * grid);
+    std::vector<long long> h((size_t)16 * grid);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), e->prof, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, e->s));
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
     const char* names[6] = {"prologue", "chain", "grid", "wait", "boundary", "lookahead"};
-    std::fprintf(stderr, "[plnmf] %s (%d CTAs) Mcycles mean/max:", what, grid);
-    for (int sct = 0; sct < 6; ++sct) {
-        double sum = 0, mx = 0;
-        for (int c = 0; c < grid; ++c) {
-            const double x = (double)h[(size_t)c * 8 + sct];
-            sum += x;
-            mx = std::max(mx, x);
+    for (int view = 0; view < 2; ++view) {
+        std::fprintf(stderr, "[plnmf] %s (%d CTAs) %s view, Mcycles mean/max:", what, grid,
+                     view ? "chain" : "look-ahead");
+        for (int sct = 0; sct < 6; ++sct) {
+            double sum = 0, mx = 0;
+            for (int c = 0; c < grid; ++c) {
+                const double x = (double)h[(size_t)c * 16 + view * 8 + sct];
+                sum += x;
+                mx = std::max(mx, x);
+            }
+            std::fprintf(stderr, " %s %.3f/%.3f", names[sct], sum / grid / 1e6, mx / 1e6);
         }
-        std::fprintf(stderr, " %s %.3f/%.3f", names[sct], sum / grid / 1e6, mx / 1e6);
+        std::fprintf(stderr, "\n");
     }
-    std::fprintf(stderr, "\n");
 }
 
 void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
@@ -265,7 +268,7 @@ void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
     } else {
         if (!e->have_ref_w) {
             e->plan_ref_w = kern::plan_reference_w(e->v, e->device);
-            if ((int64_t)e->plan_ref_w.grid * e->k > e->n_partials)
+            if (kern::exchange_partials_doubles(e->k, e->plan_ref_w.grid) > e->n_partials)
                 throw std::logic_error("plnmf_gpu: grid-norm partial buffer too small");
             e->have_ref_w = true;
         }

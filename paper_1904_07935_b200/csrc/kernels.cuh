@@ -65,6 +65,10 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
                  long long* prof = nullptr);
 
+// Workspace of the grid-wide norm exchange (replicated partials + counters).
+int64_t exchange_partials_doubles(int64_t k, int g);
+int64_t exchange_counters(int64_t k);
+
 // ---- reference (fast-hals) updaters, proj/src/hals.cpp --------------------------
 int reference_update_h(cudaStream_t s, Math m, int64_t d, int64_t k, double eps, double* ht,
                        const double* r, const double* sm);

@@ -31,6 +31,11 @@
 // column for its serial norm (hals.cpp:97-102, here a fixed-order tree).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -38,29 +43,58 @@ namespace plnmf {
 namespace {
 
 // ---------------------------------------------------------------- grid exchange
-// Deterministic grid-wide sum for column t (measured fastest of four variants,
-// tools/exchange_bench.cu: ~1.3 us on 148 SMs): each CTA stores its partial
-// into partials[t*g + cta] (NaN until written: the value is its own ready
-// flag, so no fences are needed), bumps counters[t] with a relaxed red, lane 0
-// polls the counter until all g CTAs have arrived, then the warp loads all g
-// partials at once (re-polling any still-NaN slot) and sums them in one fixed
-// order: lane l adds partials l, l+32, ... in order, then a fixed shuffle
-// tree.  Every CTA computes the bit-identical sum, run to run.
-// Called by one full warp; returns sqrt(sum) in every lane.
+// Deterministic grid-wide sum for column t.  Each CTA stores its partial into
+// every one of kReplicas copies of the column's partial array (NaN until
+// written: the value is its own ready flag, so no fences are needed) and bumps
+// every replica's arrival counter with a relaxed red; it then polls the
+// counter of replica (cta % kReplicas) until all g CTAs have arrived, loads
+// that replica's g partials at once (re-polling any slot still NaN) and sums
+// them in one fixed order — lane l adds partials l, l+32, ... in order, then a
+// fixed shuffle tree — so every CTA computes the bit-identical sum, run to
+// run.  Replication spreads the 148-way read of the same bytes over kReplicas
+// groups of L2 lines (one copy per ~18 CTAs): with a single copy, those reads
+// serialise at the L2 slices and skew the next column's arrivals by ~2.5 us
+// (measured with PLNMF_TRACE_EXCHANGE).
+// Layout: partials[(t * kReplicas + rep) * stride + cta], counters[(t * kReplicas + rep) * 64].
 constexpr int kMaxPartialsPerLane = 8;  // g <= 256 CTAs
+constexpr int kReplicas = 8;
+constexpr int kCounterStride = 64;      // 256 B between replica counters
 
-__device__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters) {
+__host__ __device__ inline int64_t partial_stride(int g) { return ((g + 31) / 32) * 32 + 32; }
+int64_t xch_partials(int64_t k, int g) { return k * kReplicas * partial_stride(g); }
+int64_t xch_counters(int64_t k) { return k * kReplicas * kCounterStride; }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Called by one full warp; returns sqrt(sum) in every lane.  trace (debug,
+// PLNMF_TRACE_EXCHANGE): per column and CTA the globaltimer at arrival, at
+// counter completion, and after the partials are read.
+__device__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
+                                unsigned long long* trace = nullptr) {
     const int lane = lane_id();
-    double* col = partials + (int64_t)t * g;
+    const int64_t stride = partial_stride(g);
+    double* base = partials + (int64_t)t * kReplicas * stride;
+    unsigned* cbase = counters + (int64_t)t * kReplicas * kCounterStride;
+    unsigned long long* tr = trace ? trace + ((int64_t)t * g + blockIdx.x) * 3 : nullptr;
+    if (tr && lane == 0) tr[0] = globaltimer();
+    if (lane < kReplicas) {
+        st_relaxed_f64(base + lane * stride + blockIdx.x, blk);
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cbase + lane * kCounterStride) : "memory");
+    }
+    const int rep = blockIdx.x % kReplicas;
     if (lane == 0) {
-        st_relaxed_f64(col + blockIdx.x, blk);
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(counters + t) : "memory");
         unsigned n;
         do {
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(counters + t) : "memory");
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(cbase + rep * kCounterStride) : "memory");
         } while (n < (unsigned)g);
+        if (tr) tr[1] = globaltimer();
     }
     __syncwarp();
+    const double* col = base + rep * stride;
     double v[kMaxPartialsPerLane];
 #pragma unroll
     for (int i = 0; i < kMaxPartialsPerLane; ++i)  // all loads in flight at once
@@ -78,6 +112,7 @@ __device__ double grid_exchange(double blk, int t, int g, double* partials, unsi
 #pragma unroll
     for (int i = 0; i < kMaxPartialsPerLane; ++i) s = dadd(s, v[i]);
     s = warp_sum_lane0(s);
+    if (tr && lane == 0) tr[2] = globaltimer();
     return __shfl_sync(0xffffffffu, __dsqrt_rn(s), 0);
 }
 
@@ -120,6 +155,8 @@ struct LookArgs {
     unsigned* counters;    // k, zeroed    (normalize)
     double* totals;        // k, NaN       (normalize)
     long long* prof;       // optional per-CTA section cycles (PLNMF_PROFILE=1)
+    int overlap;           // 1: look-ahead concurrent with the chain; 0: at the tile boundary
+    unsigned long long* trace;  // debug: exchange timestamps (k x grid x 3)
 };
 
 enum { kProfPro = 0, kProfChain = 1, kProfGrid = 2, kProfWait = 3, kProfBoundary = 4, kProfUpd = 5 };
@@ -175,25 +212,40 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // The chain warps take the HIGHEST warp ids: the issue arbiter favours
     // high warp ids, and the chain is the latency-critical path while the
     // look-ahead warps saturate the fp64 pipes.
-    const int chain_warps = min(8, max(1, (R + kWarp - 1) / kWarp));
+    // Chain = row warps (one row per thread) + for W one exchange warp that
+    // runs the grid exchange while the row warps precompute the next column's
+    // prefix terms.
+    const int row_warps = min(8, max(1, (R + kWarp - 1) / kWarp));
+    const int nrowt = row_warps * kWarp;
+    const int chain_warps = row_warps + (NORMALIZE ? 1 : 0);
     const int nchain = chain_warps * kWarp;
     const int nupd = kLThreads - nchain;
     const bool is_chain = tid >= nupd;
     const int ctid = tid - nupd;  // chain-local thread id
+    const bool is_xwarp = NORMALIZE && ctid >= nrowt;
     const int utid = tid;         // look-ahead thread id
 
-    double* acc[2] = {smem, smem + (int64_t)R * ldt};  // tile accumulators (double buffer)
-    double* oldT = acc[1] + (int64_t)R * ldt;          // R x ldt, current tile's old values
-    double* addT = oldT + (int64_t)R * ldt;            // R x ldt
-    double* sqn = addT + (int64_t)R * ldt;             // k x TQ: coeff(:, next tile's columns), zero-padded
+    // double-buffered per-tile blocks: accumulators, old values, additive term
+    const int64_t blk = (int64_t)R * ldt;
+    double* acc[2] = {smem, smem + blk};
+    double* oldB[2] = {smem + 2 * blk, smem + 3 * blk};
+    double* addB[2] = {smem + 4 * blk, smem + 5 * blk};
+    double* sqn = smem + 6 * blk;                      // k x TQ: coeff(:, next tile's columns), zero-padded
     double* sqc = sqn + (int64_t)k * TQ;               // T x T: coeff(tile, tile) of the current tile
     double* red = sqc + (int64_t)T * T;                // 48
 
+    // Section timers stay in registers (no memory traffic on the critical
+    // path) and are written once at the end; look-ahead warp 0 records the
+    // prologue / wait / look-ahead / boundary sections, chain warp 0 the chain,
+    // grid-exchange and chain-side wait sections.
     long long t0 = clock64();
+    long long sec_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     auto mark = [&](int sec) {
-        if (p.prof && (tid == 0 || tid == nupd)) {
+        if (p.prof) {
             const long long now = clock64();
-            p.prof[blockIdx.x * 8 + sec] += now - t0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i == sec) sec_t[i] += now - t0;
             t0 = now;
         }
     };
@@ -269,11 +321,23 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         }
     };
 
-    // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks
+    // old / additive values of the tile [bn, en) for this CTA's rows (coalesced rows of w doubles)
+    auto stage_tile = [&](int buf, int bn, int en, int self, int count) {
+        const int wn = en - bn;
+        for (int idx = self; idx < nrows * wn; idx += count) {
+            const int r = idx / wn, j = idx % wn;
+            const int64_t g = (r0 + r) * k + bn + j;
+            oldB[buf][r * ldt + j] = p.old_m[g];
+            addB[buf][r * ldt + j] = p.add[g];
+        }
+    };
+
+    // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks, tile-0 operands
     {
         const int e0 = min(T, k);
         load_sqn(0, e0, tid, kLThreads);
         load_sqc(0, e0, tid, kLThreads);
+        stage_tile(0, 0, e0, tid, kLThreads);
         __syncthreads();
         build_next(acc[0], 0, e0, 0, 0, kLThreads, tid);
         __syncthreads();
@@ -287,42 +351,59 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         const bool has_next = bn < k;
         double* A = acc[cur];
         if (is_chain && TMAX > 0) {
-            // ---- phase 2 of this tile, register-resident rows (one row per chain thread)
+            // ---- phase 2 of this tile, register-resident rows (one row per row thread)
+            constexpr int TM = TMAX > 0 ? TMAX : 1;
             const int r = ctid;
-            const bool own = r < nrows;
-            double x[TMAX > 0 ? TMAX : 1];
+            const bool own = !is_xwarp && r < nrows;
+            double x[TM];
             double* arow = A + r * ldt;
-            const double* addr = p.add + (r0 + r) * k + b;
+            const double* addr = addB[cur] + r * ldt;
+            const double* orow = oldB[cur] + r * ldt;
 #pragma unroll
-            for (int j = 0; j < (TMAX > 0 ? TMAX : 1); ++j)
-                x[j] = (own && j < w) ? p.old_m[(r0 + r) * k + b + j] : 0.0;
+            for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
+            double pre = 0.0;  // sum_{j < tt-1} x[j] c(j, tt), precomputed during the previous exchange
 #pragma unroll
-            for (int tt = 0; tt < (TMAX > 0 ? TMAX : 1); ++tt) {
+            for (int tt = 0; tt < TM; ++tt) {
                 if (tt < w) {
                     double val = 0.0;
                     if (own) {
                         const double a_t = arow[tt], add_t = addr[tt];
-                        double s = 0.0;
+                        double s = NORMALIZE ? pre : 0.0;
 #pragma unroll
-                        for (int j = 0; j < (TMAX > 0 ? TMAX : 1); ++j)
-                            if (j < w) s = M::madd(s, x[j], sqc[j * T + tt]);
+                        for (int j = 0; j < TM; ++j) {
+                            // scratch terms in the reference's order: new (j < tt), then old (j >= tt)
+                            const bool take = NORMALIZE ? (j + 1 >= tt && j < w) : (j < w);
+                            if (take) s = M::madd(s, x[j], sqc[j * T + tt]);
+                        }
                         val = clamp_floor(p.eps, dsub(dadd(a_t, add_t), s));
                     }
                     if (NORMALIZE) {
-                        double ss = warp_sum_lane0(M::madd(0.0, val, val));
-                        if (lane_id() == 0) red[ctid >> 5] = ss;
+                        if (!is_xwarp) {
+                            const double ss = warp_sum_lane0(M::madd(0.0, val, val));
+                            if (lane_id() == 0) red[ctid >> 5] = ss;
+                        }
                         named_sync(1, nchain);
-                        if (ctid < kWarp) {
-                            double blk = (ctid < chain_warps) ? red[ctid] : 0.0;
-                            blk = warp_sum_lane0(blk);
+                        if (is_xwarp) {
+                            double blk = 0.0;
+                            if (lane_id() == 0) {
+                                blk = red[0];
+                                for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+                            }
+                            blk = __shfl_sync(0xffffffffu, blk, 0);
                             mark(kProfChain);
                             const double norm =
-                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters);
-                            if (ctid == 0) {
+                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
+                            if (lane_id() == 0) {
                                 red[40] = norm;
                                 if (blockIdx.x == 0) p.norms[b + tt] = norm;
                             }
                             mark(kProfGrid);
+                        } else if (own && tt + 1 < w) {
+                            // next column's prefix: terms j < tt (all final) — overlaps the exchange
+                            pre = 0.0;
+#pragma unroll
+                            for (int j = 0; j < TM; ++j)
+                                if (j < tt) pre = M::madd(pre, x[j], sqc[j * T + tt + 1]);
                         }
                         named_sync(1, nchain);
                         val = clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
@@ -339,17 +420,12 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             mark(kProfChain);
         } else if (is_chain) {
             // ---- phase 2 of this tile (generic shared-memory path)
-            for (int idx = ctid; idx < nrows * w; idx += nchain) {
-                const int r = idx / w, j = idx % w;
-                const int64_t g = (r0 + r) * k + b + j;
-                oldT[r * ldt + j] = p.old_m[g];
-                addT[r * ldt + j] = p.add[g];
-            }
-            named_sync(1, nchain);
+            const double* oldT = oldB[cur];
+            const double* addT = addB[cur];
             for (int t = b; t < e; ++t) {
                 const int tt = t - b;
                 double ss = 0.0;
-                for (int r = ctid; r < nrows; r += nchain) {
+                for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
                     double* nr = A + r * ldt;
                     const double* orow = oldT + r * ldt;
                     double s = 0.0;
@@ -361,15 +437,21 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 }
                 if (NORMALIZE) {
                     // chain-group reduction (fixed tree), then the grid exchange
-                    ss = warp_sum_lane0(ss);
-                    if (lane_id() == 0) red[ctid >> 5] = ss;
+                    if (!is_xwarp) {
+                        ss = warp_sum_lane0(ss);
+                        if (lane_id() == 0) red[ctid >> 5] = ss;
+                    }
                     named_sync(1, nchain);
-                    if (ctid < kWarp) {
-                        double blk = (ctid < chain_warps) ? red[ctid] : 0.0;
-                        blk = warp_sum_lane0(blk);
+                    if (is_xwarp) {
+                        double blk = 0.0;
+                        if (lane_id() == 0) {
+                            blk = red[0];
+                            for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+                        }
+                        blk = __shfl_sync(0xffffffffu, blk, 0);
                         mark(kProfChain);
-                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
-                        if (ctid == 0) {
+                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters, p.trace);
+                        if (lane_id() == 0) {
                             red[40] = norm;
                             if (blockIdx.x == 0) p.norms[t] = norm;
                         }
@@ -377,7 +459,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     }
                     named_sync(1, nchain);
                     const double norm = red[40];
-                    for (int r = ctid; r < nrows; r += nchain) {
+                    for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
                         double* x = A + r * ldt + tt;
                         *x = clamp_floor(p.eps, __ddiv_rn(*x, norm));  // tiled.cpp:146
                     }
@@ -390,15 +472,24 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 p.out[(r0 + r) * k + b + j] = A[r * ldt + j];
             }
             mark(kProfChain);
-        } else if (has_next) {
+        } else if (has_next && p.overlap) {
             // ---- look-ahead: next tile's accumulators, minus this tile's phase-3 term
             load_sqn(bn, en, utid, nupd);
+            stage_tile(cur ^ 1, bn, en, utid, nupd);
             named_sync(2, nupd);
             build_next(acc[cur ^ 1], bn, en, b, 0, nupd, utid);
             mark(kProfUpd);
         }
         __syncthreads();
         mark(kProfWait);
+        if (has_next && !p.overlap) {
+            load_sqn(bn, en, tid, kLThreads);
+            stage_tile(cur ^ 1, bn, en, tid, kLThreads);
+            __syncthreads();
+            build_next(acc[cur ^ 1], bn, en, b, 0, kLThreads, tid);
+            __syncthreads();
+            mark(kProfUpd);
+        }
         if (has_next) {
             // ---- boundary: this tile's phase-3 term into the next tile, coeff block of the next tile
             double* An = acc[cur ^ 1];
@@ -421,6 +512,11 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         }
         cur ^= 1;
     }
+    if (p.prof && (tid == 0 || tid == nupd)) {
+        const int slot = (tid == 0) ? 0 : 8;  // look-ahead view, chain view
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p.prof[blockIdx.x * 16 + slot + i] = sec_t[i];
+    }
 }
 
 int sm_count(int device) {
@@ -431,7 +527,7 @@ int sm_count(int device) {
 
 size_t pl_smem(int64_t rows, int64_t k, int64_t tile) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
-    return sizeof(double) * (size_t)(4 * rows * (tile + 1) + k * tq + tile * tile + 48);
+    return sizeof(double) * (size_t)(6 * rows * (tile + 1) + k * tq + tile * tile + 48);
 }
 
 // ---------------------------------------------------------------- reference H
@@ -539,6 +635,9 @@ void launch_pl(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
 
 namespace kern {
 
+int64_t exchange_partials_doubles(int64_t k, int g) { return xch_partials(k, g); }
+int64_t exchange_counters(int64_t k) { return xch_counters(k); }
+
 PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device) {
     PhaseBPlan plan;
     int max_smem = 0;
@@ -568,10 +667,16 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                  long long* prof) {
     if (n <= 0 || k <= 0) return 0;
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
-               norms, partials, counters, totals, prof};
+               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : 1, nullptr};
+    static unsigned long long* trace_buf = nullptr;
+    if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
+        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 3 * 1024 * 512));
+        a.trace = trace_buf;
+    }
     if (w_update) {
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)k, s));
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF, sizeof(double) * (size_t)k * plan.grid, s));  // NaN
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)xch_counters(k), s));
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF,  // NaN
+                                         sizeof(double) * (size_t)xch_partials(k, plan.grid), s));
         if (m == Math::exact) launch_pl<MathExact, true>(s, plan, a);
         else launch_pl<MathFused, true>(s, plan, a);
     } else {
@@ -579,6 +684,34 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
         else launch_pl<MathFused, false>(s, plan, a);
     }
     PLNMF_CUDA_CHECK(cudaGetLastError());
+    if (a.trace) {
+        const int g = plan.grid;
+        std::vector<unsigned long long> h((size_t)3 * k * g);
+        PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
+                                         cudaMemcpyDeviceToHost, s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
+        double skew = 0, poll = 0, read = 0, gap = 0;
+        for (int64_t t = 0; t < k; ++t) {
+            unsigned long long amin = ~0ull, amax = 0, cmin = ~0ull, cmax = 0, rmax = 0;
+            for (int c = 0; c < g; ++c) {
+                const unsigned long long* x = &h[(size_t)(t * g + c) * 3];
+                amin = std::min(amin, x[0]); amax = std::max(amax, x[0]);
+                cmin = std::min(cmin, x[1]); cmax = std::max(cmax, x[1]);
+                rmax = std::max(rmax, x[2]);
+            }
+            skew += double(amax - amin);
+            poll += double(cmax - amax);
+            read += double(rmax - cmax);
+            if (t > 0) {
+                unsigned long long pmax = 0;
+                for (int c = 0; c < g; ++c) pmax = std::max(pmax, h[(size_t)((t - 1) * g + c) * 3 + 2]);
+                gap += double(amin - pmax);
+            }
+        }
+        std::fprintf(stderr, "[plnmf] exchange trace (ns/column): arrival skew %.0f, last-arrival->all-complete %.0f, "
+                     "complete->partials read %.0f, prev-done->first-arrival %.0f\n",
+                     skew / k, poll / k, read / k, gap / (k - 1));
+    }
     return 1;
 }
 
@@ -612,8 +745,9 @@ int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v
                        double* w, const double* p, const double* q, double* norms, double* partials,
                        unsigned* counters, double* totals) {
     if (v <= 0 || k <= 0) return 0;
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)k, s));
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF, sizeof(double) * (size_t)k * plan.grid, s));  // NaN
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)xch_counters(k), s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF,  // NaN
+                                     sizeof(double) * (size_t)xch_partials(k, plan.grid), s));
     RefWArgs a{v, (int)k, eps, plan.rows_per_cta, w, p, q, norms, partials, counters, totals};
     void* args[] = {&a};
     const void* fn = (m == Math::exact) ? (const void*)ref_update_w_kernel<MathExact>

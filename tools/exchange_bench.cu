@@ -28,11 +28,31 @@ constexpr int MAXL = 8;
 // variant 1: relaxed atomic + NaN-sentinel partials (no fences), last sums, poll total
 // variant 2: all CTAs poll all NaN-sentinel partials (with backoff)
 // variant 3: relaxed red arrival; lane 0 polls counter; then all read partials (NaN-guarded)
+__device__ volatile int g_stop;
+
 template <int VAR>
-__global__ void xkernel(int ncol, double* partials, unsigned* counters, double* totals, double* out, int sleep_ns) {
+__global__ void xkernel(int ncol, double* partials, unsigned* counters, double* totals, double* out, int sleep_ns,
+                        int gap, int busy) {
     const int g = gridDim.x, lane = threadIdx.x & 31;
     double acc = 0;
+    if (busy && threadIdx.x >= 64) {  // sibling warps: fp64 work + L2 loads until warp 0 is done
+        double x = threadIdx.x, y = 1.0000001;
+        const double* src = partials;
+        int it = 0;
+        while (!g_stop) {
+            for (int i = 0; i < 64; ++i) x = fma(x, y, 1e-9);
+            if (busy > 1) x += src[(threadIdx.x * 97 + it * 131) % 4096];
+            ++it;
+        }
+        if (threadIdx.x == 64) out[blockIdx.x + gridDim.x] = x;
+        return;
+    }
     for (int t = 0; t < ncol; ++t) {
+        if (gap) {
+            const long long t0 = clock64();
+            while (clock64() - t0 < gap) {
+            }
+        }
         const double blk = 1.0 + blockIdx.x + t;
         if (threadIdx.x < 32) {
             double* col = partials + (size_t)t * g;
@@ -108,9 +128,14 @@ __global__ void xkernel(int ncol, double* partials, unsigned* counters, double* 
             }
             acc += norm;
         }
-        __syncthreads();
+        if (busy) asm volatile("bar.sync 1, 64;"); else __syncthreads();
     }
     if (threadIdx.x == 0) out[blockIdx.x] = acc;
+    if (busy && threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd((unsigned*)&counters[ncol], 1u);
+        if (atomicAdd((unsigned*)&counters[ncol], 0u) == (unsigned)gridDim.x) g_stop = 1;
+    }
 }
 
 int main() {
@@ -122,31 +147,41 @@ int main() {
     cudaMalloc(&partials, sizeof(double) * ncol * g);
     cudaMalloc(&totals, sizeof(double) * ncol);
     cudaMalloc(&out, sizeof(double) * g);
-    cudaMalloc(&counters, sizeof(unsigned) * ncol);
+    cudaMalloc(&counters, sizeof(unsigned) * (ncol + 1));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const char* names[4] = {"acq_rel atomic + last sums", "relaxed atomic + NaN partials", "all poll all partials",
                             "red arrive + counter poll + read"};
-    for (int var = 0; var < 4; ++var)
-        for (int sl : {0, 16, 64}) {
-            float best = 1e9;
-            for (int rep = 0; rep < 5; ++rep) {
-                cudaMemset(partials, 0xFF, sizeof(double) * ncol * g);
-                cudaMemset(totals, 0xFF, sizeof(double) * ncol);
-                cudaMemset(counters, 0, sizeof(unsigned) * ncol);
-                cudaEventRecord(a);
-                void* args[] = {(void*)&ncol, &partials, &counters, &totals, &out, &sl};
-                void* fn = var == 0 ? (void*)xkernel<0> : var == 1 ? (void*)xkernel<1> : var == 2 ? (void*)xkernel<2> : (void*)xkernel<3>;
-                cudaLaunchCooperativeKernel(fn, g, 512, args, 0, 0);
-                cudaEventRecord(b);
-                cudaEventSynchronize(b);
-                float ms;
-                cudaEventElapsedTime(&ms, a, b);
-                if (ms < best) best = ms;
-            }
-            printf("%-36s sleep=%3d ns: %7.3f us per exchange (%s)\n", names[var], sl, best * 1e3 / ncol,
-                   cudaGetErrorString(cudaGetLastError()));
+    struct Cfg { int var, sleep, gap, busy, smem; const char* what; };
+    Cfg cfgs[] = {{3, 0, 0, 0, 0, "red+poll, back to back"},
+                  {3, 0, 2800, 0, 0, "red+poll, 2.8k-cycle gap"},
+                  {3, 0, 2800, 0, 133000, "red+poll, gap, 130KB smem"},
+                  {3, 0, 2800, 1, 0, "red+poll, gap, 14 busy fp64 warps"},
+                  {3, 0, 2800, 2, 0, "red+poll, gap, busy fp64+L2 loads"},
+                  {1, 0, 2800, 0, 0, "relaxed atomic last-sums, gap"},
+                  {1, 0, 2800, 2, 0, "relaxed atomic last-sums, gap, busy+L2"},
+                  {2, 64, 2800, 0, 0, "all-poll sleep64, gap"}};
+    for (auto c : cfgs) {
+        float best = 1e9;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaMemset(partials, 0xFF, sizeof(double) * ncol * g);
+            cudaMemset(totals, 0xFF, sizeof(double) * ncol);
+            cudaMemset(counters, 0, sizeof(unsigned) * (ncol + 1));
+            int zero = 0;
+            cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
+            void* args[] = {(void*)&ncol, &partials, &counters, &totals, &out, &c.sleep, &c.gap, &c.busy};
+            void* fn = c.var == 0 ? (void*)xkernel<0> : c.var == 1 ? (void*)xkernel<1> : c.var == 2 ? (void*)xkernel<2> : (void*)xkernel<3>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+            cudaEventRecord(a);
+            cudaLaunchCooperativeKernel(fn, g, 512, args, c.smem, 0);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
         }
+        printf("%-42s: %7.3f us per column (%s)\n", c.what, best * 1e3 / ncol, cudaGetErrorString(cudaGetLastError()));
+    }
     return 0;
 }
