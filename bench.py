@@ -49,45 +49,44 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self._stop = index, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.index, self.proc, self.out = index, None, ""
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = [[x.strip() for x in ln.split(",")] for ln in self.out.splitlines() if ln.count(",") >= 5]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda x: float(x) if x.replace(".", "", 1).isdigit() else None  # noqa: E731
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[2:6]) if v.strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def make_input():
@@ -272,28 +271,35 @@ def engine_arm(args):
 
 def e2e_arm(P, a, eng, cfg, alg, args, torch):
     """Each step = one drop-in iterate() call through the C-ABI with HOST
-    factors (plnmf_gpu_iterate_host): H2D of W and Ht, one FAST-HALS iteration
-    with the reference's error evaluations, D2H of W, Ht and the trace."""
+    factors in pinned memory (plnmf_gpu_iterate_host): H2D of W and Ht, one
+    FAST-HALS iteration with the reference's two error evaluations (initial +
+    after the iteration, solver.cpp:75-76,94-95), D2H of W, Ht and the trace."""
     import ctypes as C
     from paper_1904_07935_b200 import _lib as L
     f = eng.get_factors()
-    w = np.asfortranarray(f.w)
-    ht = np.asfortranarray(f.ht)
+    # pinned, column-major (Fortran) host factors: a (K, n) row-major pinned tensor viewed transposed
+    tw = torch.empty((K, V), dtype=torch.float64, pin_memory=True)
+    th = torch.empty((K, D), dtype=torch.float64, pin_memory=True)
+    w, ht = tw.numpy().T, th.numpy().T
+    w[...] = f.w
+    ht[...] = f.ht
+    assert w.flags.f_contiguous and ht.flags.f_contiguous
     c = cfg.to_c()
     buf = P._TraceBuf(1)
     lib = L.lib()
     ptr = lambda x: x.ctypes.data_as(L.P_f64)  # noqa: E731
     for _ in range(2):
         P._check(lib.plnmf_gpu_iterate_host(eng._h, C.byref(c), int(alg), ptr(w), ptr(ht), C.byref(buf.c)))
+    n = max(5, args.steps // 2)
     t0 = time.perf_counter()
-    n = max(3, args.steps // 2)
     for _ in range(n):
         P._check(lib.plnmf_gpu_iterate_host(eng._h, C.byref(c), int(alg), ptr(w), ptr(ht), C.byref(buf.c)))
     dt = time.perf_counter() - t0
     fb = 8 * (V + D) * K
-    return {"value": n / dt, "unit": "iters/s", "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb + 8 * 3,
-            "what": "plnmf_gpu_iterate_host(max_iters=1): upload W,Ht (col-major f64), iterate incl. the "
-                    "reference's initial + final error evaluation, download W,Ht; host wall clock"}
+    tb = 8 * 3 + 8 * 12  # initial error + one trace record
+    return {"value": n / dt, "unit": "iters/s", "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb + tb,
+            "what": "plnmf_gpu_iterate_host(max_iters=1) on pinned host W,Ht (col-major f64): upload, one "
+                    "iteration incl. the reference's initial + final error evaluation, download; host wall clock"}
 
 
 def ncu_traffic(kernel):
@@ -308,7 +314,7 @@ def ncu_traffic(kernel):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--math", default="exact", choices=["exact", "fused"])
