@@ -5,10 +5,11 @@
 // `omp simd reduction` runs as two SSE2 lanes (even / odd row offsets, an odd
 // tail row into lane 0, combined as (lane0 + 0.0) + lane1 — objdump of the
 // Release linalg.o), and the blocks are added to g in order.  Here one CTA
-// computes a 32x32 tile of entries for one 2048-row block, each thread a 4x4
-// register tile with separate even/odd accumulators, rows streamed through
+// computes a 32x32 tile of entries for one 2048-row block and one lane parity
+// (even or odd rows), each thread a 4x4 register tile, rows streamed through
 // shared memory in ascending order — the same per-entry operation sequence.
-// A second kernel adds the per-block partials in block order and mirrors.
+// A second kernel combines the lanes and adds the per-block partials in block
+// order, then mirrors.
 //
 // dense_a_ht / dense_at_w: replace gemm(..., a.dense(), ...) at
 // proj/src/hals.cpp:29,43 (accumulate_nn / accumulate_tn, linalg.cpp:45-79)
@@ -36,6 +37,11 @@ __device__ __forceinline__ void decode_upper(int p, int ntile, int& ta, int& tb)
     tb = ta + p;
 }
 
+// One CTA = one 32x32 tile of (a, b) entries, one 2048-row block, ONE lane
+// parity: lane 0 (even row offsets) and lane 1 (odd) are independent
+// sequential sums in the reference, so they run in separate CTAs (twice the
+// parallelism, half the registers); the combine kernel adds them as
+// (lane0 + 0.0) + lane1 exactly like the compiled reduction.
 template <class M>
 __global__ void __launch_bounds__(kGramThreads) gram_block_kernel(int64_t n, int k,
                                                                   const double* __restrict__ m,
@@ -45,29 +51,32 @@ __global__ void __launch_bounds__(kGramThreads) gram_block_kernel(int64_t n, int
     __shared__ double Bs[kGramRows][kGramTile];
     int ta, tb;
     decode_upper(blockIdx.x, ntile, ta, tb);
-    const int64_t blk = blockIdx.y;
+    const int64_t blk = blockIdx.y >> 1;
+    const int parity = blockIdx.y & 1;
     const int64_t v0 = blk * kGramBlock;
     const int64_t v1 = (v0 + kGramBlock < n) ? v0 + kGramBlock : n;
+    // rows of this parity in [v0, v1): v0 + parity + 2i, i < cnt
+    const int64_t cnt = (v1 - v0 - parity + 1) / 2;
     const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
     const int a0 = ta * kGramTile, b0 = tb * kGramTile;
 
-    double e[4][4], o[4][4];
+    double acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) e[i][j] = o[i][j] = 0.0;
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
 
-    for (int64_t r0 = v0; r0 < v1; r0 += kGramRows) {
-        const int nr = (int)((v1 - r0) < kGramRows ? (v1 - r0) : kGramRows);
+    for (int64_t i0 = 0; i0 < cnt; i0 += kGramRows) {
+        const int nr = (int)((cnt - i0) < kGramRows ? (cnt - i0) : kGramRows);
         for (int idx = threadIdx.x; idx < kGramRows * kGramTile; idx += kGramThreads) {
             const int rr = idx / kGramTile, cc = idx % kGramTile;
             const bool rok = rr < nr;
-            As[rr][cc] = (rok && a0 + cc < k) ? m[(r0 + rr) * k + a0 + cc] : 0.0;
-            Bs[rr][cc] = (rok && b0 + cc < k) ? m[(r0 + rr) * k + b0 + cc] : 0.0;
+            const int64_t row = v0 + parity + 2 * (i0 + rr);
+            As[rr][cc] = (rok && a0 + cc < k) ? m[row * k + a0 + cc] : 0.0;
+            Bs[rr][cc] = (rok && b0 + cc < k) ? m[row * k + b0 + cc] : 0.0;
         }
         __syncthreads();
-        // r0 - v0 is a multiple of kGramRows (even): offset parity == rr parity.
-        for (int rr = 0; rr < nr; rr += 2) {
+        for (int rr = 0; rr < nr; ++rr) {
             double av[4], bv[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) av[i] = As[rr][ty + 8 * i];
@@ -76,27 +85,17 @@ __global__ void __launch_bounds__(kGramThreads) gram_block_kernel(int64_t n, int
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) e[i][j] = M::madd(e[i][j], av[i], bv[j]);
-            if (rr + 1 < nr) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) av[i] = As[rr + 1][ty + 8 * i];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) bv[j] = Bs[rr + 1][tx + 8 * j];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) o[i][j] = M::madd(o[i][j], av[i], bv[j]);
-            }
+                for (int j = 0; j < 4; ++j) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
         }
         __syncthreads();
     }
-    double* pb = part + blk * (int64_t)k * k;
+    double* pb = part + (int64_t)blockIdx.y * k * k;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int a = a0 + ty + 8 * i, b = b0 + tx + 8 * j;
-            if (a < k && b < k) pb[(int64_t)a * k + b] = dadd(dadd(e[i][j], 0.0), o[i][j]);
+            if (a < k && b < k) pb[(int64_t)a * k + b] = acc[i][j];
         }
 }
 
@@ -107,8 +106,13 @@ __global__ void gram_combine_kernel(int k, int64_t nblk, const double* __restric
     if (idx >= (int64_t)k * k) return;
     const int a = (int)(idx / k), b = (int)(idx % k);
     if (a > b) return;
+    const int64_t kk = (int64_t)k * k;
     double s = 0.0;
-    for (int64_t blk = 0; blk < nblk; ++blk) s = dadd(s, part[(blk * k + a) * k + b]);
+    for (int64_t blk = 0; blk < nblk; ++blk) {
+        const double lane0 = part[(2 * blk) * kk + (int64_t)a * k + b];
+        const double lane1 = part[(2 * blk + 1) * kk + (int64_t)a * k + b];
+        s = dadd(s, dadd(dadd(lane0, 0.0), lane1));  // g += (lane0 + 0.0) + lane1
+    }
     g[(int64_t)a * k + b] = s;
     g[(int64_t)b * k + a] = s;
 }
@@ -232,7 +236,7 @@ namespace kern {
 
 int64_t gram_scratch_doubles(int64_t n, int64_t k) {
     const int64_t nblk = (n + kGramBlock - 1) / kGramBlock;
-    return (nblk > 0 ? nblk : 1) * k * k;
+    return 2 * (nblk > 0 ? nblk : 1) * k * k;  // one K x K partial per block and lane
 }
 
 int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double* g,
@@ -244,7 +248,7 @@ int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double
         return 0;
     }
     const int ntile = (int)((k + kGramTile - 1) / kGramTile);
-    const dim3 grid((unsigned)(ntile * (ntile + 1) / 2), (unsigned)nblk);
+    const dim3 grid((unsigned)(ntile * (ntile + 1) / 2), (unsigned)(2 * nblk));
     if (m == Math::exact)
         gram_block_kernel<MathExact><<<grid, kGramThreads, 0, s>>>(n, (int)k, mat, scratch, ntile);
     else

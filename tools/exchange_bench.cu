@@ -30,7 +30,7 @@ constexpr int MAXL = 8;
 // variant 3: relaxed red arrival; lane 0 polls counter; then all read partials (NaN-guarded)
 __device__ volatile int g_stop;
 
-template <int VAR>
+template <int VAR, int REP = 8>
 __global__ void xkernel(int ncol, double* partials, unsigned* counters, double* totals, double* out, int sleep_ns,
                         int gap, int busy) {
     const int g = gridDim.x, lane = threadIdx.x & 31;
@@ -105,6 +105,33 @@ __global__ void xkernel(int ncol, double* partials, unsigned* counters, double* 
                 double s = 0;
                 for (int i = 0; i < MAXL; ++i) s += v[i];
                 norm = __shfl_sync(~0u, wsum(s), 0);
+            } else if (VAR == 4 || VAR == 5) {
+                const int stride = ((g + 31) / 32) * 32 + 32;
+                double* base = partials + (size_t)t * REP * stride;
+                unsigned* cb = counters + (size_t)t * REP * 64;
+                if (lane < REP) {
+                    str(base + lane * stride + blockIdx.x, blk);
+                    if (VAR == 4) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cb + lane * 64) : "memory");
+                }
+                const int rep = blockIdx.x % REP;
+                if (VAR == 4 && lane == 0)
+                    while (ldru(cb + rep * 64) < (unsigned)g) {
+                    }
+                __syncwarp();
+                const double* c2 = base + rep * stride;
+                double v[MAXL];
+                for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? ldr(c2 + lane + 32 * i) : 0.0;
+                for (;;) {
+                    bool pend = false;
+                    for (int i = 0; i < MAXL; ++i) pend |= isnan(v[i]);
+                    if (!__any_sync(~0u, pend)) break;
+                    if (sleep_ns) __nanosleep(sleep_ns);
+                    for (int i = 0; i < MAXL; ++i)
+                        if (isnan(v[i])) v[i] = ldr(c2 + lane + 32 * i);
+                }
+                double s = 0;
+                for (int i = 0; i < MAXL; ++i) s += v[i];
+                norm = __shfl_sync(~0u, wsum(s), 0);
             } else {
                 if (lane == 0) {
                     str(col + blockIdx.x, blk);
@@ -133,8 +160,8 @@ __global__ void xkernel(int ncol, double* partials, unsigned* counters, double* 
     if (threadIdx.x == 0) out[blockIdx.x] = acc;
     if (busy && threadIdx.x == 0) {
         __threadfence();
-        atomicAdd((unsigned*)&counters[ncol], 1u);
-        if (atomicAdd((unsigned*)&counters[ncol], 0u) == (unsigned)gridDim.x) g_stop = 1;
+        atomicAdd((unsigned*)&counters[ncol * 32 * 64], 1u);
+        if (atomicAdd((unsigned*)&counters[ncol * 32 * 64], 0u) == (unsigned)gridDim.x) g_stop = 1;
     }
 }
 
@@ -144,34 +171,35 @@ int main() {
     const int ncol = 240, g = sms;
     double *partials, *totals, *out;
     unsigned* counters;
-    cudaMalloc(&partials, sizeof(double) * ncol * g);
+    cudaMalloc(&partials, sizeof(double) * ncol * 32 * (g + 64));
     cudaMalloc(&totals, sizeof(double) * ncol);
     cudaMalloc(&out, sizeof(double) * g);
-    cudaMalloc(&counters, sizeof(unsigned) * (ncol + 1));
+    cudaMalloc(&counters, sizeof(unsigned) * (ncol * 32 * 64 + 1));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const char* names[4] = {"acq_rel atomic + last sums", "relaxed atomic + NaN partials", "all poll all partials",
                             "red arrive + counter poll + read"};
-    struct Cfg { int var, sleep, gap, busy, smem; const char* what; };
-    Cfg cfgs[] = {{3, 0, 0, 0, 0, "red+poll, back to back"},
-                  {3, 0, 2800, 0, 0, "red+poll, 2.8k-cycle gap"},
-                  {3, 0, 2800, 0, 133000, "red+poll, gap, 130KB smem"},
-                  {3, 0, 2800, 1, 0, "red+poll, gap, 14 busy fp64 warps"},
-                  {3, 0, 2800, 2, 0, "red+poll, gap, busy fp64+L2 loads"},
-                  {1, 0, 2800, 0, 0, "relaxed atomic last-sums, gap"},
-                  {1, 0, 2800, 2, 0, "relaxed atomic last-sums, gap, busy+L2"},
-                  {2, 64, 2800, 0, 0, "all-poll sleep64, gap"}};
+    struct Cfg { int var, sleep, gap, busy, smem; const char* what; void* fn; };
+    Cfg cfgs[] = {{3, 0, 2800, 0, 0, "counter+read, 1 copy", (void*)xkernel<3>},
+                  {4, 0, 2800, 0, 0, "counter+read, 8 replicas", (void*)xkernel<4, 8>},
+                  {4, 0, 2800, 0, 0, "counter+read, 16 replicas", (void*)xkernel<4, 16>},
+                  {5, 0, 2800, 0, 0, "all-poll, 8 replicas", (void*)xkernel<5, 8>},
+                  {5, 32, 2800, 0, 0, "all-poll, 8 replicas, sleep32", (void*)xkernel<5, 8>},
+                  {5, 0, 2800, 0, 0, "all-poll, 16 replicas", (void*)xkernel<5, 16>},
+                  {5, 0, 2800, 0, 0, "all-poll, 32 replicas", (void*)xkernel<5, 32>},
+                  {5, 0, 0, 0, 0, "all-poll, 16 replicas, no gap", (void*)xkernel<5, 16>},
+                  {4, 0, 0, 0, 0, "counter+read, 8 replicas, no gap", (void*)xkernel<4, 8>}};
     for (auto c : cfgs) {
         float best = 1e9;
         for (int rep = 0; rep < 3; ++rep) {
-            cudaMemset(partials, 0xFF, sizeof(double) * ncol * g);
+            cudaMemset(partials, 0xFF, sizeof(double) * ncol * 32 * (g + 64));
             cudaMemset(totals, 0xFF, sizeof(double) * ncol);
-            cudaMemset(counters, 0, sizeof(unsigned) * (ncol + 1));
+            cudaMemset(counters, 0, sizeof(unsigned) * (ncol * 32 * 64 + 1));
             int zero = 0;
             cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
             void* args[] = {(void*)&ncol, &partials, &counters, &totals, &out, &c.sleep, &c.gap, &c.busy};
-            void* fn = c.var == 0 ? (void*)xkernel<0> : c.var == 1 ? (void*)xkernel<1> : c.var == 2 ? (void*)xkernel<2> : (void*)xkernel<3>;
+            void* fn = c.fn;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
             cudaEventRecord(a);
             cudaLaunchCooperativeKernel(fn, g, 512, args, c.smem, 0);
