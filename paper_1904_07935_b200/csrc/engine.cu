@@ -60,6 +60,8 @@ struct plnmf_gpu_engine {
     std::vector<cudaEvent_t> events;  // per-phase timing pool
     long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
     int64_t prof_n = 0;
+    double* qpanel = nullptr;         // coeff column panels of the tiled updates
+    int64_t qpanel_n = 0;
 };
 
 namespace {
@@ -183,6 +185,11 @@ void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
     if (e->plan_tile == tile) return;
     e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device);
     e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device);
+    const int64_t qn = kern::qpanel_doubles(e->k, tile);
+    if (qn > e->qpanel_n) {
+        e->qpanel = dalloc<double>(e, qn);
+        e->qpanel_n = qn;
+    }
     if (kern::exchange_partials_doubles(e->k, e->plan_w.grid) > e->n_partials)
         throw std::logic_error("plnmf_gpu: grid-norm partial buffer too small");
     e->plan_tile = tile;
@@ -244,7 +251,8 @@ void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         ensure_plans(e, cfg.tile_size);
         long long* prof = prof_buffer(e, e->plan_h.grid);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_h, e->d, e->k, cfg.tile_size, cfg.epsilon, false,
-                                          e->ht, e->h_new, e->sm, e->r, nullptr, nullptr, nullptr, nullptr, prof);
+                                          e->ht, e->h_new, e->sm, e->r, nullptr, nullptr, nullptr, nullptr, prof,
+                                          e->qpanel);
         if (prof) prof_report(e, "H update", e->plan_h.grid);
         std::swap(e->ht, e->h_new);  // ht.swap(ws.h_new), tiled.cpp:213
         e->update_macs += tiled_macs(e->d, e->k, cfg.tile_size, false);
@@ -261,7 +269,7 @@ void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         long long* prof = prof_buffer(e, e->plan_w.grid);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true,
                                           e->w, e->w_new, e->q, e->p, e->norms, e->partials, e->counters, e->totals,
-                                          prof);
+                                          prof, e->qpanel);
         if (prof) prof_report(e, "W update", e->plan_w.grid);
         std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
         e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);

@@ -54,16 +54,26 @@ struct PhaseBPlan {
     int64_t rows_per_cta = 0;
     size_t smem = 0;         // dynamic shared memory bytes
     bool cooperative = false;
+    bool streaming = false;  // fallback: tile operands streamed from global (stream.cu)
+    bool stage_ops = true;   // look-ahead: tile old/add operands staged in shared memory
+    bool sqn_smem = true;    // look-ahead: next tile's coeff panel staged in shared memory
 };
+// Global scratch for the coeff column panels of one tiled update.
+int64_t qpanel_doubles(int64_t k, int64_t tile);
 // One look-ahead kernel per update: init_new_accumulator (:28-50), phase 1
 // (:52-65), and per tile phase 2 (:67-156) + phase 3 (:158-174).  w_update =>
 // init scales by the diagonal and every column is L2-normalised with a
 // grid-wide exchange (cooperative persistent launch, one CTA per SM).
 PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
+// Streaming fallback (stream.cu): phase A + one persistent streaming launch.
+PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
+int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
+                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
+                  const double* add, double* norms, double* partials, unsigned* counters);
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
-                 long long* prof = nullptr);
+                 long long* prof, double* qpanel);
 
 // Workspace of the grid-wide norm exchange (replicated partials + counters).
 int64_t exchange_partials_doubles(int64_t k, int g);

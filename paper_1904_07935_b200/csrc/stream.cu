@@ -1,0 +1,252 @@
+// Streaming tiled (PL-NMF) update — the general fallback of the look-ahead
+// kernel (update.cu) for shapes whose per-SM tile state does not fit in shared
+// memory (large V and/or K: C3, C5).  Same per-element operation order as the
+// reference (proj/src/tiled.cpp), so H is bit-identical and W differs only in
+// the column-norm reduction order, exactly like the look-ahead path.
+//
+//   stream_phase_a  init_new_accumulator (:28-50) + phase1_left_contributions
+//                   (:52-65) as a register-tiled SIMT GEMM into nb (global).
+//   stream_update   one persistent launch (cooperative for W): for each tile,
+//                   phase 2 (:67-156) one thread per row with the row's tile
+//                   operands streamed from global/L1, the column norm through
+//                   the grid exchange, then phase 3 (:158-174) over the CTA's
+//                   own rows (4 independent columns per thread).
+#include "common.cuh"
+#include "exchange.cuh"
+#include "kernels.cuh"
+
+namespace plnmf {
+namespace {
+
+constexpr int kTileRows = 64, kTileCols = 64, kTileK = 16, kPhaseAThreads = 256;
+
+template <class M>
+__global__ void __launch_bounds__(kPhaseAThreads) stream_phase_a_kernel(int64_t n, int k, int tile,
+                                                                        int use_diag,
+                                                                        const double* __restrict__ old_m,
+                                                                        const double* __restrict__ coeff,
+                                                                        double* __restrict__ nb) {
+    __shared__ double As[kTileK][kTileRows + 1];  // old(r0+rr, k0+kk) at [kk][rr]
+    __shared__ double Bs[kTileK][kTileCols];      // -coeff(k0+kk, c0+cc)
+    const int c0 = blockIdx.x * kTileCols;
+    const int64_t r0 = (int64_t)blockIdx.y * kTileRows;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+    int estart[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = c0 + tx + 16 * j;
+        const int e = (c / tile + 1) * tile;  // first column right of c's tile
+        estart[j] = e < k ? e : k;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t r = r0 + ty + 16 * i;
+            const int c = c0 + tx + 16 * j;
+            double x = 0.0;
+            if (r < n && c < k) {
+                x = old_m[r * k + c];
+                if (use_diag) x = dmul(x, coeff[(int64_t)c * k + c]);  // tiled.cpp:44
+            }
+            acc[i][j] = x;
+        }
+    const int kbeg = ((c0 / tile + 1) * tile) < k ? (c0 / tile + 1) * tile : k;
+    for (int k0 = kbeg; k0 < k; k0 += kTileK) {
+        for (int idx = threadIdx.x; idx < kTileK * kTileRows; idx += kPhaseAThreads) {
+            const int rr = idx / kTileK, kk = idx % kTileK;
+            As[kk][rr] = (r0 + rr < n && k0 + kk < k) ? old_m[(r0 + rr) * k + k0 + kk] : 0.0;
+            const int kb = idx / kTileCols, cc = idx % kTileCols;
+            // f = alpha * b(kk, j) with alpha = -1 (tiled.cpp:58-60, linalg.cpp:52)
+            Bs[kb][cc] = (k0 + kb < k && c0 + cc < k) ? -1.0 * coeff[(int64_t)(k0 + kb) * k + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (k - k0) < kTileK ? (k - k0) : kTileK;
+        for (int kk = 0; kk < kmax; ++kk) {
+            const int kabs = k0 + kk;
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (kabs >= estart[j]) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[i][j] = M::madd(acc[i][j], bv[j], av[i]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t r = r0 + ty + 16 * i;
+            const int c = c0 + tx + 16 * j;
+            if (r < n && c < k) nb[r * k + c] = acc[i][j];
+        }
+}
+
+constexpr int kSThreads = 512;
+
+struct StreamArgs {
+    int64_t n;
+    int k;
+    int tile;
+    double eps;
+    int64_t rows_per_cta;
+    const double* old_m;
+    double* nb;
+    const double* coeff;
+    const double* add;
+    double* norms;
+    double* partials;
+    unsigned* counters;
+};
+
+template <class M, bool NORMALIZE>
+__global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs p) {
+    __shared__ double red[48];
+    const int k = p.k, T = p.tile, tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_cta;
+    const int64_t r1 = (r0 + p.rows_per_cta < p.n) ? r0 + p.rows_per_cta : p.n;
+    for (int b = 0; b < k; b += T) {
+        const int e = (b + T < k) ? b + T : k, w = e - b;
+        // ---- phase 2: columns in order; each thread keeps the same rows throughout
+        for (int t = b; t < e; ++t) {
+            const int tt = t - b;
+            double ss = 0.0;
+            for (int64_t r = r0 + tid; r < r1; r += kSThreads) {
+                const double* nr = p.nb + r * k + b;
+                const double* orow = p.old_m + r * k + b;
+                const double a_t = nr[tt], add_t = p.add[r * k + t];
+                double s = 0.0;
+                // operands in batches of 8 independent loads (new for j < tt, old for j >= tt),
+                // then the scratch terms in the reference's order
+                for (int j0 = 0; j0 < w; j0 += 8) {
+                    double x[8], c[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        x[u] = (j < w) ? (j < tt ? nr[j] : orow[j]) : 0.0;
+                        c[u] = (j < w) ? __ldg(p.coeff + (int64_t)(b + j) * k + t) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (j0 + u < w) s = M::madd(s, x[u], c[u]);
+                }
+                const double val = clamp_floor(p.eps, dsub(dadd(a_t, add_t), s));
+                p.nb[r * k + t] = val;
+                if (NORMALIZE) ss = M::madd(ss, val, val);
+            }
+            if (NORMALIZE) {
+                const double blk = block_sum(ss, red);
+                if (tid < kWarp) {
+                    const double nrm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
+                    if (tid == 0) {
+                        red[40] = nrm;
+                        if (blockIdx.x == 0) p.norms[t] = nrm;
+                    }
+                }
+                __syncthreads();
+                const double norm = red[40];
+                for (int64_t r = r0 + tid; r < r1; r += kSThreads) {
+                    double* x = p.nb + r * k + t;
+                    *x = clamp_floor(p.eps, __ddiv_rn(*x, norm));  // tiled.cpp:146
+                }
+            }
+        }
+        __syncthreads();
+        // ---- phase 3 over this CTA's rows: nb(r,c) += (-coeff(kk,c)) * nb(r,kk), kk in the tile
+        const int rest = k - e;
+        if (rest > 0) {
+            const int ng = (rest + 3) / 4;
+            const int64_t items = (r1 - r0) * ng;
+            for (int64_t it = tid; it < items; it += kSThreads) {
+                const int64_t r = r0 + it / ng;
+                const int c0 = e + (int)(it % ng) * 4;
+                double* row = p.nb + r * k;
+                double a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = (c0 + u < k) ? row[c0 + u] : 0.0;
+                for (int j0 = 0; j0 < w; j0 += 8) {
+                    double x[8];
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) x[v] = (j0 + v < w) ? row[b + j0 + v] : 0.0;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        if (j0 + v < w) {
+                            const double* cf = p.coeff + (int64_t)(b + j0 + v) * k + c0;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (c0 + u < k) a[u] = M::madd(a[u], -1.0 * __ldg(cf + u), x[v]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (c0 + u < k) row[c0 + u] = a[u];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int sm_count(int device) {
+    int n = 0;
+    PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    return n;
+}
+
+}  // namespace
+
+namespace kern {
+
+PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device) {
+    (void)k;
+    (void)tile;
+    PhaseBPlan plan;
+    const int sms = sm_count(device);
+    if (normalize) {
+        plan.grid = sms;  // one resident CTA per SM, grid exchange per column
+        plan.cooperative = true;
+    } else {
+        plan.grid = (int)std::min<int64_t>(std::max<int64_t>(1, (n + 63) / 64), 4 * (int64_t)sms);
+    }
+    plan.rows_per_cta = n > 0 ? (n + plan.grid - 1) / plan.grid : 1;
+    plan.streaming = true;
+    return plan;
+}
+
+int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
+                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
+                  const double* add, double* norms, double* partials, unsigned* counters) {
+    if (n <= 0 || k <= 0) return 0;
+    // phase A: init + phase 1 into `out` (used as the accumulator nb)
+    const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
+    if (m == Math::exact)
+        stream_phase_a_kernel<MathExact><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
+    else
+        stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    StreamArgs a{n, (int)k, (int)tile, eps, plan.rows_per_cta, old_m, out, coeff, add, norms, partials, counters};
+    const dim3 grid((unsigned)plan.grid), block(kSThreads);
+    if (w_update) {
+        exchange_reset(s, k, plan.grid, partials, counters);
+        void* args[] = {&a};
+        const void* fn = (m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
+                                            : (const void*)stream_update_kernel<MathFused, true>;
+        PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+    } else if (m == Math::exact) {
+        stream_update_kernel<MathExact, false><<<grid, block, 0, s>>>(a);
+    } else {
+        stream_update_kernel<MathFused, false><<<grid, block, 0, s>>>(a);
+    }
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return 2;
+}
+
+}  // namespace kern
+}  // namespace plnmf

@@ -37,84 +37,11 @@
 #include <vector>
 
 #include "common.cuh"
+#include "exchange.cuh"
 #include "kernels.cuh"
 
 namespace plnmf {
 namespace {
-
-// ---------------------------------------------------------------- grid exchange
-// Deterministic grid-wide sum for column t.  Each CTA stores its partial into
-// every one of kReplicas copies of the column's partial array (NaN until
-// written: the value is its own ready flag, so no fences are needed) and bumps
-// every replica's arrival counter with a relaxed red; it then polls the
-// counter of replica (cta % kReplicas) until all g CTAs have arrived, loads
-// that replica's g partials at once (re-polling any slot still NaN) and sums
-// them in one fixed order — lane l adds partials l, l+32, ... in order, then a
-// fixed shuffle tree — so every CTA computes the bit-identical sum, run to
-// run.  Replication spreads the 148-way read of the same bytes over kReplicas
-// groups of L2 lines (one copy per ~18 CTAs): with a single copy, those reads
-// serialise at the L2 slices and skew the next column's arrivals by ~2.5 us
-// (measured with PLNMF_TRACE_EXCHANGE).
-// Layout: partials[(t * kReplicas + rep) * stride + cta], counters[(t * kReplicas + rep) * 64].
-constexpr int kMaxPartialsPerLane = 8;  // g <= 256 CTAs
-constexpr int kReplicas = 8;
-constexpr int kCounterStride = 64;      // 256 B between replica counters
-
-__host__ __device__ inline int64_t partial_stride(int g) { return ((g + 31) / 32) * 32 + 32; }
-int64_t xch_partials(int64_t k, int g) { return k * kReplicas * partial_stride(g); }
-int64_t xch_counters(int64_t k) { return k * kReplicas * kCounterStride; }
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Called by one full warp; returns sqrt(sum) in every lane.  trace (debug,
-// PLNMF_TRACE_EXCHANGE): per column and CTA the globaltimer at arrival, at
-// counter completion, and after the partials are read.
-__device__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
-                                unsigned long long* trace = nullptr) {
-    const int lane = lane_id();
-    const int64_t stride = partial_stride(g);
-    double* base = partials + (int64_t)t * kReplicas * stride;
-    unsigned* cbase = counters + (int64_t)t * kReplicas * kCounterStride;
-    unsigned long long* tr = trace ? trace + ((int64_t)t * g + blockIdx.x) * 3 : nullptr;
-    if (tr && lane == 0) tr[0] = globaltimer();
-    if (lane < kReplicas) {
-        st_relaxed_f64(base + lane * stride + blockIdx.x, blk);
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cbase + lane * kCounterStride) : "memory");
-    }
-    const int rep = blockIdx.x % kReplicas;
-    if (lane == 0) {
-        unsigned n;
-        do {
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(cbase + rep * kCounterStride) : "memory");
-        } while (n < (unsigned)g);
-        if (tr) tr[1] = globaltimer();
-    }
-    __syncwarp();
-    const double* col = base + rep * stride;
-    double v[kMaxPartialsPerLane];
-#pragma unroll
-    for (int i = 0; i < kMaxPartialsPerLane; ++i)  // all loads in flight at once
-        v[i] = (lane + kWarp * i < g) ? ld_relaxed_f64(col + lane + kWarp * i) : 0.0;
-    for (;;) {
-        bool pending = false;
-#pragma unroll
-        for (int i = 0; i < kMaxPartialsPerLane; ++i) pending |= isnan(v[i]);
-        if (!__any_sync(0xffffffffu, pending)) break;
-#pragma unroll
-        for (int i = 0; i < kMaxPartialsPerLane; ++i)
-            if (isnan(v[i])) v[i] = ld_relaxed_f64(col + lane + kWarp * i);
-    }
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < kMaxPartialsPerLane; ++i) s = dadd(s, v[i]);
-    s = warp_sum_lane0(s);
-    if (tr && lane == 0) tr[2] = globaltimer();
-    return __shfl_sync(0xffffffffu, __dsqrt_rn(s), 0);
-}
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -157,6 +84,9 @@ struct LookArgs {
     long long* prof;       // optional per-CTA section cycles (PLNMF_PROFILE=1)
     int overlap;           // 1: look-ahead concurrent with the chain; 0: at the tile boundary
     unsigned long long* trace;  // debug: exchange timestamps (k x grid x 3)
+    const double* qpanel;  // [tile][k][TQ] column panels of coeff (zero-padded), built per update
+    int stage_ops;         // 1: the tile's old/add operands are staged in shared memory
+    int sqn_smem;          // 1: the next tile's coeff panel is staged in shared memory
 };
 
 enum { kProfPro = 0, kProfChain = 1, kProfGrid = 2, kProfWait = 3, kProfBoundary = 4, kProfUpd = 5 };
@@ -200,7 +130,7 @@ __device__ __forceinline__ void row_panel(double (&acc)[C], const double* __rest
 // exactly the operand the reference reads: new for j < t, old for j >= t), so
 // each column's scratch sum is a pure register DADD chain.  TMAX = 0: generic
 // shared-memory path for tiles wider than 32.
-template <class M, bool NORMALIZE, int TMAX>
+template <class M, bool NORMALIZE, int TMAX, bool STAGE, bool SQN>
 __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     extern __shared__ double smem[];
     const int T = p.tile, k = p.k, ldt = T + 1;
@@ -225,13 +155,15 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     const bool is_xwarp = NORMALIZE && ctid >= nrowt;
     const int utid = tid;         // look-ahead thread id
 
-    // double-buffered per-tile blocks: accumulators, old values, additive term
+    // double-buffered per-tile blocks: accumulators and (optionally) the old
+    // values / additive term; optionally the next tile's coeff panel.  Shapes
+    // too large for shared memory read those from global (L1) instead.
     const int64_t blk = (int64_t)R * ldt;
     double* acc[2] = {smem, smem + blk};
     double* oldB[2] = {smem + 2 * blk, smem + 3 * blk};
     double* addB[2] = {smem + 4 * blk, smem + 5 * blk};
-    double* sqn = smem + 6 * blk;                      // k x TQ: coeff(:, next tile's columns), zero-padded
-    double* sqc = sqn + (int64_t)k * TQ;               // T x T: coeff(tile, tile) of the current tile
+    double* sqn = smem + (STAGE ? 6 : 2) * blk;  // k x TQ: coeff(:, next tile's columns), zero-padded
+    double* sqc = sqn + (SQN ? (int64_t)k * TQ : 0);  // T x T: coeff(tile, tile) of the current tile
     double* red = sqc + (int64_t)T * T;                // 48
 
     // Section timers stay in registers (no memory traffic on the critical
@@ -250,6 +182,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         }
     };
 
+    // the coeff panel of the tile starting at column bn: shared copy or global panel
+    auto Qn = [&](int bn) -> const double* {
+        return SQN ? sqn : p.qpanel + (int64_t)(bn / T) * k * TQ;
+    };
     // Builds the accumulators of the tile [bn, en) except the phase-3 term of
     // the tile just before it: init + phase 1 + phase 3 from [0, b_prev).
     // Run by `count` threads, this one being number `self`.
@@ -257,6 +193,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // row (8 independent chains); one load of the row operand feeds 8 MACs and
     // the 8 coefficients come as 4 vector LDS.128 from sqn (ld TQ, even).
     auto build_next = [&](double* dst, int bn, int en, int bprev, int first, int count, int self) {
+        const double* Q = Qn(bn);
         if (TMAX > 0) {
             constexpr int C8 = 8;
             const int wn = en - bn;
@@ -271,11 +208,11 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     if (cq + u < wn) {
                         const int c = bn + cq + u;
                         const double o = p.old_m[g + c];
-                        a[u] = p.use_diag ? dmul(o, sqn[c * TQ + cq + u]) : o;
+                        a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
                     }
                 }
-                row_panel<M, C8>(a, p.old_m + g, en, k, sqn, TQ, cq);   // phase 1
-                row_panel<M, C8>(a, p.out + g, 0, bprev, sqn, TQ, cq);  // phase 3, tiles before the previous
+                row_panel<M, C8>(a, p.old_m + g, en, k, Q, TQ, cq);   // phase 1
+                row_panel<M, C8>(a, p.out + g, 0, bprev, Q, TQ, cq);  // phase 3, tiles before the previous
 #pragma unroll
                 for (int u = 0; u < C8; ++u)
                     if (cq + u < wn) dst[r * ldt + cq + u] = a[u];
@@ -295,11 +232,11 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 if (u < wq) {
                     const int c = bn + cq + u;
                     const double o = p.old_m[g + c];
-                    a[u] = p.use_diag ? dmul(o, sqn[c * TQ + cq + u]) : o;
+                    a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
                 }
             }
-            accumulate_quad<M>(a, p.old_m + g, en, k, sqn, TQ, cq, wq);  // phase 1
-            accumulate_quad<M>(a, p.out + g, 0, bprev, sqn, TQ, cq, wq);  // phase 3, tiles before the previous
+            accumulate_quad<M>(a, p.old_m + g, en, k, Q, TQ, cq, wq);  // phase 1
+            accumulate_quad<M>(a, p.out + g, 0, bprev, Q, TQ, cq, wq);  // phase 3, tiles before the previous
 #pragma unroll
             for (int u = 0; u < kLQuad; ++u)
                 if (u < wq) dst[r * ldt + cq + u] = a[u];
@@ -307,11 +244,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         (void)first;
     };
     auto load_sqn = [&](int bn, int en, int self, int count) {
-        const int wn = en - bn;
-        for (int idx = self; idx < k * TQ; idx += count) {
-            const int kk = idx / TQ, j = idx % TQ;
-            sqn[kk * TQ + j] = (j < wn) ? p.coeff[(int64_t)kk * k + bn + j] : 0.0;
-        }
+        (void)en;
+        if (!SQN) return;
+        const double* src = p.qpanel + (int64_t)(bn / T) * k * TQ;
+        for (int idx = self; idx < k * TQ; idx += count) sqn[idx] = src[idx];
     };
     auto load_sqc = [&](int b, int e, int self, int count) {
         const int w = e - b;
@@ -323,6 +259,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
 
     // old / additive values of the tile [bn, en) for this CTA's rows (coalesced rows of w doubles)
     auto stage_tile = [&](int buf, int bn, int en, int self, int count) {
+        if (!STAGE) return;
         const int wn = en - bn;
         for (int idx = self; idx < nrows * wn; idx += count) {
             const int r = idx / wn, j = idx % wn;
@@ -357,17 +294,20 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             const bool own = !is_xwarp && r < nrows;
             double x[TM];
             double* arow = A + r * ldt;
-            const double* addr = addB[cur] + r * ldt;
-            const double* orow = oldB[cur] + r * ldt;
+            const double* addr = STAGE ? addB[cur] + r * ldt : p.add + (r0 + r) * k + b;
+            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
 #pragma unroll
             for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
             double pre = 0.0;  // sum_{j < tt-1} x[j] c(j, tt), precomputed during the previous exchange
+            double add_next = own ? addr[0] : 0.0;  // additive term, loaded one column ahead
 #pragma unroll
             for (int tt = 0; tt < TM; ++tt) {
                 if (tt < w) {
                     double val = 0.0;
+                    const double add_t = add_next;
+                    if (own && tt + 1 < w) add_next = addr[tt + 1];  // in flight across this column's exchange
                     if (own) {
-                        const double a_t = arow[tt], add_t = addr[tt];
+                        const double a_t = arow[tt];
                         double s = NORMALIZE ? pre : 0.0;
 #pragma unroll
                         for (int j = 0; j < TM; ++j) {
@@ -420,18 +360,19 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             mark(kProfChain);
         } else if (is_chain) {
             // ---- phase 2 of this tile (generic shared-memory path)
-            const double* oldT = oldB[cur];
-            const double* addT = addB[cur];
+            const double* oldT = STAGE ? oldB[cur] : p.old_m + r0 * k + b;
+            const double* addT = STAGE ? addB[cur] : p.add + r0 * k + b;
+            const int64_t ldo = STAGE ? ldt : k;
             for (int t = b; t < e; ++t) {
                 const int tt = t - b;
                 double ss = 0.0;
                 for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
                     double* nr = A + r * ldt;
-                    const double* orow = oldT + r * ldt;
+                    const double* orow = oldT + r * ldo;
                     double s = 0.0;
                     for (int j = 0; j < tt; ++j) s = M::madd(s, nr[j], sqc[j * T + tt]);
                     for (int j = tt; j < w; ++j) s = M::madd(s, orow[j], sqc[j * T + tt]);
-                    const double val = clamp_floor(p.eps, dsub(dadd(nr[tt], addT[r * ldt + tt]), s));
+                    const double val = clamp_floor(p.eps, dsub(dadd(nr[tt], addT[r * ldo + tt]), s));
                     nr[tt] = val;
                     if (NORMALIZE) ss = M::madd(ss, val, val);
                 }
@@ -501,7 +442,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
 #pragma unroll
                 for (int u = 0; u < kLQuad; ++u) a[u] = (u < wq) ? An[r * ldt + cq + u] : 0.0;
                 // src row = finished tile values, indexed by absolute kk in [b, e)
-                accumulate_quad<M>(a, A + r * ldt - b, b, e, sqn, TQ, cq, wq);
+                accumulate_quad<M>(a, A + r * ldt - b, b, e, Qn(bn), TQ, cq, wq);
 #pragma unroll
                 for (int u = 0; u < kLQuad; ++u)
                     if (u < wq) An[r * ldt + cq + u] = a[u];
@@ -525,9 +466,22 @@ int sm_count(int device) {
     return n;
 }
 
-size_t pl_smem(int64_t rows, int64_t k, int64_t tile) {
+size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
-    return sizeof(double) * (size_t)(6 * rows * (tile + 1) + k * tq + tile * tile + 48);
+    return sizeof(double) * (size_t)((stage_ops ? 6 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
+                                     tile * tile + 48);
+}
+
+// qpanel[tau][kk][j] = coeff(kk, b_tau + j) for j < width(tau), 0 up to TQ.
+__global__ void qpanel_kernel(int k, int tile, int tq, const double* __restrict__ coeff, double* __restrict__ qp) {
+    const int64_t gamma = (k + tile - 1) / tile;
+    const int64_t total = gamma * k * tq;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tau = i / ((int64_t)k * tq);
+        const int kk = (int)((i / tq) % k), j = (int)(i % tq);
+        const int64_t b = tau * tile;
+        qp[i] = (j < tile && b + j < k) ? coeff[(int64_t)kk * k + b + j] : 0.0;
+    }
 }
 
 // ---------------------------------------------------------------- reference H
@@ -609,9 +563,9 @@ __global__ void __launch_bounds__(kRefWThreads) ref_update_w_kernel(RefWArgs a) 
     }
 }
 
-template <class M, bool NORM, int TMAX>
+template <class M, bool NORM, int TMAX, bool STAGE, bool SQN>
 void launch_pl_t(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
-    auto fn = pl_update_kernel<M, NORM, TMAX>;
+    auto fn = pl_update_kernel<M, NORM, TMAX, STAGE, SQN>;
     PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
     const dim3 grid((unsigned)plan.grid), block(kLThreads);
     if (NORM) {
@@ -622,13 +576,22 @@ void launch_pl_t(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
     }
 }
 
+// Shared-memory variants: both staged, panel only, neither (the planner
+// never picks "operands staged, panel global").
+template <class M, bool NORM, int TMAX>
+void launch_pl_s(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
+    if (plan.stage_ops) launch_pl_t<M, NORM, TMAX, true, true>(s, plan, a);
+    else if (plan.sqn_smem) launch_pl_t<M, NORM, TMAX, false, true>(s, plan, a);
+    else launch_pl_t<M, NORM, TMAX, false, false>(s, plan, a);
+}
+
 // Register-resident chains need one row per chain thread (<= 256 rows per CTA).
 template <class M, bool NORM>
 void launch_pl(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
     const bool regs = plan.rows_per_cta <= 8 * kWarp;
-    if (regs && a.tile <= 16) launch_pl_t<M, NORM, 16>(s, plan, a);
-    else if (regs && a.tile <= 32) launch_pl_t<M, NORM, 32>(s, plan, a);
-    else launch_pl_t<M, NORM, 0>(s, plan, a);
+    if (regs && a.tile <= 16) launch_pl_s<M, NORM, 16>(s, plan, a);
+    else if (regs && a.tile <= 32) launch_pl_s<M, NORM, 32>(s, plan, a);
+    else launch_pl_s<M, NORM, 0>(s, plan, a);
 }
 
 }  // namespace
@@ -644,39 +607,64 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
     PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     const int sms = sm_count(device);
     int64_t rpc = n > 0 ? (n + sms - 1) / sms : 1;  // one SM's share of rows
+    if (std::getenv("PLNMF_FORCE_STREAMING")) return plan_stream_update(n, k, tile, normalize, device);
+    // shared-memory variants, most staged first
+    const bool variants[3][2] = {{true, true}, {false, true}, {false, false}};
+    auto pick = [&](int64_t rows) -> int {
+        for (int v = 0; v < 3; ++v)
+            if (pl_smem(rows, k, tile, variants[v][0], variants[v][1]) <= (size_t)max_smem) return v;
+        return -1;
+    };
+    int v = -1;
     if (normalize) {
-        // persistent + grid-synchronised: exactly one resident CTA per SM
-        if (pl_smem(rpc, k, tile) > (size_t)max_smem || rpc > 8 * 32 * 4)
-            throw std::invalid_argument(
-                "update_w_tiled: one SM cannot hold its share of rows for this V and tile_size on one GPU; "
-                "use a smaller tile_size or shard V across GPUs");
+        // persistent + grid-synchronised: exactly one resident CTA per SM with
+        // one SM's rows (one row per chain thread); otherwise the streaming path
+        v = rpc <= 8 * 32 ? pick(rpc) : -1;
+        if (v < 0) return plan_stream_update(n, k, tile, normalize, device);
         plan.grid = sms;
         plan.cooperative = true;
     } else {
-        while (rpc > 1 && pl_smem(rpc, k, tile) > (size_t)max_smem) rpc = (rpc + 1) / 2;
+        while (rpc > 1 && pick(rpc) != 0 && rpc > 32) rpc = (rpc + 1) / 2;
+        v = pick(rpc);
+        if (v < 0) return plan_stream_update(n, k, tile, normalize, device);
         plan.grid = (int)((n + rpc - 1) / rpc);
     }
+    plan.stage_ops = variants[v][0];
+    plan.sqn_smem = variants[v][1];
     plan.rows_per_cta = rpc;
-    plan.smem = pl_smem(rpc, k, tile);
+    plan.smem = pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem);
     return plan;
+}
+
+int64_t qpanel_doubles(int64_t k, int64_t tile) {
+    const int64_t tq = (tile + 7) & ~int64_t(7);
+    return ((k + tile - 1) / tile) * k * tq;
 }
 
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
-                 long long* prof) {
+                 long long* prof, double* qpanel) {
     if (n <= 0 || k <= 0) return 0;
+    if (plan.streaming)
+        return stream_update(s, m, plan, n, k, tile, eps, w_update, old_m, out, coeff, add, norms, partials,
+                             counters);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
-               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : 1, nullptr};
+               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : 1, nullptr,
+               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0};
+    {
+        const int tq = (int)((tile + 7) & ~int64_t(7));
+        qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(
+            (int)k, (int)tile, tq, coeff, qpanel);
+        PLNMF_CUDA_CHECK(cudaGetLastError());
+    }
     static unsigned long long* trace_buf = nullptr;
     if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
         if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 3 * 1024 * 512));
         a.trace = trace_buf;
     }
     if (w_update) {
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)xch_counters(k), s));
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF,  // NaN
-                                         sizeof(double) * (size_t)xch_partials(k, plan.grid), s));
+        exchange_reset(s, k, plan.grid, partials, counters);
         if (m == Math::exact) launch_pl<MathExact, true>(s, plan, a);
         else launch_pl<MathFused, true>(s, plan, a);
     } else {
@@ -745,9 +733,7 @@ int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v
                        double* w, const double* p, const double* q, double* norms, double* partials,
                        unsigned* counters, double* totals) {
     if (v <= 0 || k <= 0) return 0;
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (size_t)xch_counters(k), s));
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(partials, 0xFF,  // NaN
-                                     sizeof(double) * (size_t)xch_partials(k, plan.grid), s));
+    exchange_reset(s, k, plan.grid, partials, counters);
     RefWArgs a{v, (int)k, eps, plan.rows_per_cta, w, p, q, norms, partials, counters, totals};
     void* args[] = {&a};
     const void* fn = (m == Math::exact) ? (const void*)ref_update_w_kernel<MathExact>
