@@ -62,6 +62,13 @@ struct plnmf_gpu_engine {
     int64_t prof_n = 0;
     double* qpanel = nullptr;         // coeff column panels of the tiled updates
     int64_t qpanel_n = 0;
+
+    // sharded engine (multi-GPU): local rows [v_lo, v_lo+v) of W and [d_lo, d_lo+d) of Ht
+    bool shard = false;
+    int world = 1;
+    int64_t vfull = 0, dfull = 0, v_lo = 0, d_lo = 0;
+    double *w_full = nullptr, *ht_full = nullptr;           // gather buffers (row-major V x K, D x K)
+    double *col_ss = nullptr, *world_ss = nullptr, *col_partials = nullptr;
 };
 
 namespace {
@@ -157,7 +164,8 @@ void precompute_h(plnmf_gpu_engine* e) {
         e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
     }
     if (e->sparse)
-        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
+        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->shard ? e->w_full : e->w,
+                                      e->k, e->r);
     else
         e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
     if (need_s) {
@@ -174,7 +182,8 @@ void precompute_w(plnmf_gpu_engine* e) {
     PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
     e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
     if (e->sparse)
-        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p);
+        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
+                                      e->k, e->p);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
     PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
@@ -713,6 +722,176 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which, con
             PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         }
         if (which == PLNMF_PRODUCT_S) e->s_valid = false;
+    });
+}
+
+// ---- sharded engine --------------------------------------------------------------------
+plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int64_t v, int64_t d, int64_t v_lo, int64_t v_hi,
+                                    int64_t d_lo, int64_t d_hi, int64_t nnz_rows, const int64_t* rp_rows,
+                                    const int64_t* ci_rows, const double* val_rows, int64_t nnz_cols,
+                                    const int64_t* rp_cols, const int64_t* ci_cols, const double* val_cols,
+                                    double a_norm_sq, int64_t rank, plnmf_gpu_engine** out) {
+    plnmf_gpu_engine* e = nullptr;
+    const plnmf_status st = guarded([&] {
+        if (!out) throw std::invalid_argument("plnmf_gpu_create_shard: null output");
+        if (world < 1) throw std::invalid_argument("plnmf_gpu_create_shard: world must be >= 1");
+        if (v_lo < 0 || v_hi < v_lo || v_hi > v || d_lo < 0 || d_hi < d_lo || d_hi > d)
+            throw std::invalid_argument("plnmf_gpu_create_shard: shard ranges out of bounds");
+        const int64_t vl = v_hi - v_lo, dl = d_hi - d_lo;
+        validate_csr(vl, d, nnz_rows, rp_rows, ci_rows, val_rows);
+        validate_csr(dl, v, nnz_cols, rp_cols, ci_cols, val_cols);
+        if (d > INT32_MAX || v > INT32_MAX) throw std::invalid_argument("plnmf_gpu_create_shard: dimensions exceed int32");
+        e = new plnmf_gpu_engine();
+        setup_common(e, device, rank);
+        e->shard = true;
+        e->world = world;
+        e->vfull = v;
+        e->dfull = d;
+        e->v_lo = v_lo;
+        e->d_lo = d_lo;
+        e->v = vl;
+        e->d = dl;
+        e->nnz = nnz_rows;
+        e->sparse = true;
+        e->a2 = a_norm_sq;
+        auto upload = [&](int64_t rows, int64_t nnz, const int64_t* rp, const int64_t* ci, const double* val,
+                          int64_t*& drp, int32_t*& dci, double*& dval) {
+            std::vector<int32_t> ci32(nnz > 0 ? nnz : 1);
+            for (int64_t i = 0; i < nnz; ++i) ci32[i] = (int32_t)ci[i];
+            drp = dalloc<int64_t>(e, rows + 1);
+            dci = dalloc<int32_t>(e, nnz);
+            dval = dalloc<double>(e, nnz);
+            PLNMF_CUDA_CHECK(cudaMemcpy(drp, rp, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice));
+            if (nnz > 0) {
+                PLNMF_CUDA_CHECK(cudaMemcpy(dci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+                PLNMF_CUDA_CHECK(cudaMemcpy(dval, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+            }
+        };
+        upload(vl, nnz_rows, rp_rows, ci_rows, val_rows, e->rp, e->ci, e->val);
+        upload(dl, nnz_cols, rp_cols, ci_cols, val_cols, e->trp, e->tci, e->tval);
+        alloc_workspace(e);
+        e->w_full = dalloc<double>(e, v * rank);
+        e->ht_full = dalloc<double>(e, d * rank);
+        e->col_ss = dalloc<double>(e, 1);
+        e->world_ss = dalloc<double>(e, world);
+        e->col_partials = dalloc<double>(e, 512);
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->w_full, 0, sizeof(double) * v * rank, e->s));
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht_full, 0, sizeof(double) * d * rank, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        *out = e;
+    });
+    if (st != PLNMF_OK) release(e);
+    return st;
+}
+
+plnmf_status plnmf_gpu_buffer(plnmf_gpu_engine* e, plnmf_buffer which, void** ptr, int64_t* rows, int64_t* cols) {
+    return guarded([&] {
+        check_engine(e);
+        double* p = nullptr;
+        int64_t r = 0, c = e->k;
+        switch (which) {
+            case PLNMF_BUF_W: p = e->w; r = e->v; break;
+            case PLNMF_BUF_HT: p = e->ht; r = e->d; break;
+            case PLNMF_BUF_W_FULL: p = e->w_full; r = e->vfull; break;
+            case PLNMF_BUF_HT_FULL: p = e->ht_full; r = e->dfull; break;
+            case PLNMF_BUF_S: p = e->sm; r = e->k; break;
+            case PLNMF_BUF_Q: p = e->q; r = e->k; break;
+            case PLNMF_BUF_P: p = e->p; r = e->v; break;
+            case PLNMF_BUF_R: p = e->r; r = e->d; break;
+            case PLNMF_BUF_COLUMN_SS: p = e->col_ss; r = 1; c = 1; break;
+            case PLNMF_BUF_WORLD_SS: p = e->world_ss; r = e->world; c = 1; break;
+            default: throw std::invalid_argument("plnmf_gpu_buffer: unknown buffer");
+        }
+        if (!p) throw std::invalid_argument("plnmf_gpu_buffer: buffer not available (not a sharded engine?)");
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        if (ptr) *ptr = p;
+        if (rows) *rows = r;
+        if (cols) *cols = c;
+    });
+}
+
+plnmf_status plnmf_gpu_shard_publish(plnmf_gpu_engine* e) {
+    return guarded([&] {
+        check_engine(e);
+        if (!e->shard) throw std::invalid_argument("plnmf_gpu_shard_publish: not a sharded engine");
+        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->w_full + e->v_lo * e->k, e->w, sizeof(double) * e->v * e->k,
+                                         cudaMemcpyDeviceToDevice, e->s));
+        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->ht_full + e->d_lo * e->k, e->ht, sizeof(double) * e->d * e->k,
+                                         cudaMemcpyDeviceToDevice, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        e->s_valid = false;
+    });
+}
+
+static void check_tiled(plnmf_gpu_engine* e, const plnmf_config* cfg) {
+    check_engine(e);
+    if (!cfg) throw std::invalid_argument("plnmf_gpu_w_*: null config");
+    plnmf::validate_config(*cfg);
+    if (cfg->rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
+    check_tile(*cfg, e->k);
+}
+
+plnmf_status plnmf_gpu_w_begin(plnmf_gpu_engine* e, const plnmf_config* cfg) {
+    return guarded([&] {
+        check_tiled(e, cfg);
+        e->launches += kern::stream_phase_a(e->s, e->math, e->v, e->k, cfg->tile_size, true, e->w, e->q, e->w_new);
+    });
+}
+
+plnmf_status plnmf_gpu_w_column_step(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t) {
+    return guarded([&] {
+        check_tiled(e, cfg);
+        if (t < 0 || t >= e->k) throw std::invalid_argument("plnmf_gpu_w_column_step: column out of range");
+        if (!e->col_partials) {
+            e->col_ss = dalloc<double>(e, 1);
+            e->world_ss = dalloc<double>(e, std::max(1, e->world));
+            e->col_partials = dalloc<double>(e, 512);
+        }
+        const int64_t b = (t / cfg->tile_size) * cfg->tile_size, en = std::min(e->k, b + cfg->tile_size);
+        e->launches += kern::shard_col_step(e->s, e->math, e->v, e->k, b, en, t, cfg->epsilon, e->w, e->w_new, e->q,
+                                            e->p, e->col_partials, e->col_ss);
+    });
+}
+
+plnmf_status plnmf_gpu_w_normalize(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t) {
+    return guarded([&] {
+        check_tiled(e, cfg);
+        if (t < 0 || t >= e->k) throw std::invalid_argument("plnmf_gpu_w_normalize: column out of range");
+        if (!e->shard) {  // single engine: this rank's partial is the world
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->world_ss, e->col_ss, sizeof(double), cudaMemcpyDeviceToDevice, e->s));
+        }
+        e->launches += kern::shard_normalize(e->s, e->v, e->k, t, cfg->epsilon, e->shard ? e->world : 1, e->world_ss,
+                                             e->w_new, e->norms);
+    });
+}
+
+plnmf_status plnmf_gpu_w_phase3(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t tile_begin) {
+    return guarded([&] {
+        check_tiled(e, cfg);
+        if (tile_begin < 0 || tile_begin >= e->k || tile_begin % cfg->tile_size)
+            throw std::invalid_argument("plnmf_gpu_w_phase3: not a tile start");
+        const int64_t en = std::min(e->k, tile_begin + cfg->tile_size);
+        e->launches += kern::shard_phase3(e->s, e->math, e->v, e->k, tile_begin, en, e->w_new, e->q);
+    });
+}
+
+plnmf_status plnmf_gpu_w_end(plnmf_gpu_engine* e) {
+    return guarded([&] {
+        check_engine(e);
+        std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
+        e->s_valid = false;
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    });
+}
+
+plnmf_status plnmf_gpu_local_pw(plnmf_gpu_engine* e, double* out) {
+    return guarded([&] {
+        check_engine(e);
+        if (!out) throw std::invalid_argument("plnmf_gpu_local_pw: null output");
+        e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
+        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars, e->scalars, sizeof(double), cudaMemcpyDeviceToHost, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        *out = e->host_scalars[0];
     });
 }
 

@@ -70,6 +70,16 @@ PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                   const double* add, double* norms, double* partials, unsigned* counters);
+// init_new_accumulator + phase1_left_contributions into nb (tiled.cpp:28-65).
+int stream_phase_a(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
+                   const double* coeff, double* nb);
+// Column-stepped W update pieces for the sharded engine (shard.cu).
+int shard_col_step(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t b, int64_t e, int64_t t, double eps,
+                   const double* old_m, double* nb, const double* coeff, const double* add, double* block_partials,
+                   double* ss_out);
+int shard_normalize(cudaStream_t s, int64_t n, int64_t k, int64_t t, double eps, int world,
+                    const double* world_partials, double* nb, double* norms);
+int shard_phase3(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t b, int64_t e, double* nb, const double* coeff);
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,

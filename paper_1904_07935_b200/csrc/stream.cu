@@ -204,6 +204,18 @@ int sm_count(int device) {
 
 namespace kern {
 
+int stream_phase_a(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
+                   const double* coeff, double* nb) {
+    if (n <= 0 || k <= 0) return 0;
+    const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
+    if (m == Math::exact)
+        stream_phase_a_kernel<MathExact><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, use_diag, old_m, coeff, nb);
+    else
+        stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, use_diag, old_m, coeff, nb);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return 1;
+}
+
 PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device) {
     (void)k;
     (void)tile;
