@@ -225,8 +225,8 @@ void check_tile(const plnmf_config& cfg, int64_t k) {
 
 long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
     if (!std::getenv("PLNMF_PROFILE")) return nullptr;
-    if (!e->prof || e->prof_n < 16 * (int64_t)grid) {
-        e->prof_n = 16 * (int64_t)grid;
+    if (!e->prof || e->prof_n < 24 * (int64_t)grid) {
+        e->prof_n = 24 * (int64_t)grid;
         e->prof = dalloc<long long>(e, e->prof_n);
     }
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->prof, 0, sizeof(long long) * e->prof_n, e->s));
@@ -234,17 +234,17 @@ long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
 }
 
 void prof_report(plnmf_gpu_engine* e, const char* what, int grid) {
-    std::vector<long long> h((size_t)16 * grid);
+    std::vector<long long> h((size_t)24 * grid);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), e->prof, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, e->s));
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-    const char* names[6] = {"prologue", "chain", "grid", "wait", "boundary", "lookahead"};
-    for (int view = 0; view < 2; ++view) {
+    const char* names[8] = {"prologue", "chain", "grid", "wait", "boundary", "lookahead/pre", "div", "dot"};
+    for (int view = 0; view < 3; ++view) {
         std::fprintf(stderr, "[plnmf] %s (%d CTAs) %s view, Mcycles mean/max:", what, grid,
-                     view ? "chain" : "look-ahead");
-        for (int sct = 0; sct < 6; ++sct) {
+                     view == 0 ? "look-ahead" : view == 1 ? "chain" : "exchange-warp");
+        for (int sct = 0; sct < 8; ++sct) {
             double sum = 0, mx = 0;
             for (int c = 0; c < grid; ++c) {
-                const double x = (double)h[(size_t)c * 16 + view * 8 + sct];
+                const double x = (double)h[(size_t)c * 24 + view * 8 + sct];
                 sum += x;
                 mx = std::max(mx, x);
             }

@@ -36,7 +36,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Called by one full warp; returns sqrt(sum) in every lane.  trace (debug,
-// PLNMF_TRACE_EXCHANGE): per column and CTA the globaltimer at arrival, at
+// PLNMF_TRACE_EXCHANGE): per column and CTA the SM clock at arrival, at
 // counter completion, and after the partials are read.
 __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
                                 unsigned long long* trace = nullptr) {
@@ -45,7 +45,7 @@ __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double
     double* base = partials + (int64_t)t * kReplicas * stride;
     unsigned* cbase = counters + (int64_t)t * kReplicas * kCounterStride;
     unsigned long long* tr = trace ? trace + ((int64_t)t * g + blockIdx.x) * 3 : nullptr;
-    if (tr && lane == 0) tr[0] = globaltimer();
+    if (tr && lane == 0) tr[0] = clock64();
     if (lane < kReplicas) {
         st_relaxed_f64(base + lane * stride + blockIdx.x, blk);
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cbase + lane * kCounterStride) : "memory");
@@ -56,7 +56,7 @@ __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double
         do {
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(cbase + rep * kCounterStride) : "memory");
         } while (n < (unsigned)g);
-        if (tr) tr[1] = globaltimer();
+        if (tr) tr[1] = clock64();
     }
     __syncwarp();
     const double* col = base + rep * stride;
@@ -77,7 +77,7 @@ __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double
 #pragma unroll
     for (int i = 0; i < kMaxPartialsPerLane; ++i) s = dadd(s, v[i]);
     s = warp_sum_lane0(s);
-    if (tr && lane == 0) tr[2] = globaltimer();
+    if (tr && lane == 0) tr[2] = clock64();
     return __shfl_sync(0xffffffffu, __dsqrt_rn(s), 0);
 }
 

@@ -57,6 +57,8 @@ struct PhaseBPlan {
     bool streaming = false;  // fallback: tile operands streamed from global (stream.cu)
     bool stage_ops = true;   // look-ahead: tile old/add operands staged in shared memory
     bool sqn_smem = true;    // look-ahead: next tile's coeff panel staged in shared memory
+    int kc = 0;              // look-ahead GEMM: operand chunk width staged by cp.async (0: unstaged path)
+    int kst = 0;             // look-ahead GEMM: chunk ring depth
 };
 // Global scratch for the coeff column panels of one tiled update.
 int64_t qpanel_doubles(int64_t k, int64_t tile);

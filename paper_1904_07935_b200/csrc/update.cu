@@ -39,426 +39,20 @@
 #include "common.cuh"
 #include "exchange.cuh"
 #include "kernels.cuh"
+#include "lookahead.cuh"
+#include "update_kern.cuh"
 
 namespace plnmf {
+namespace upd {
+extern template void launch_pl<MathExact, true>(cudaStream_t, const kern::PhaseBPlan&, LookArgs&);
+extern template void launch_pl<MathExact, false>(cudaStream_t, const kern::PhaseBPlan&, LookArgs&);
+extern template void launch_pl<MathFused, true>(cudaStream_t, const kern::PhaseBPlan&, LookArgs&);
+extern template void launch_pl<MathFused, false>(cudaStream_t, const kern::PhaseBPlan&, LookArgs&);
+}  // namespace upd
 namespace {
-
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// ---------------------------------------------------------------- look-ahead tiled update
-// One persistent kernel per factor update (W: cooperative, one CTA per SM, one
-// grid exchange per column; H: ordinary launch).  A CTA owns R consecutive
-// rows.  Its warps split into
-//   chain warps  (one thread per row): phase 2 of tile s, column by column —
-//                the latency-critical recurrence;
-//   update warps : meanwhile build tile s+1's accumulators
-//                  acc(r,c) = init(old(r,c)[*coeff(c,c)])           tiled.cpp:44
-//                           + sum_{kk >= e_{s+1}} -coeff(kk,c)*old(r,kk)   phase 1, :58-60
-//                           + sum_{kk <  b_s}     -coeff(kk,c)*out(r,kk)   phase 3 of tiles < s
-//                  — each term in the reference's order (kk ascending).
-// At the tile boundary all warps add tile s's phase-3 term to tile s+1 and
-// the next tile starts.  Finished tiles are written to `out` (global) where
-// later tiles' update warps read them.  The per-element operation sequence is
-// exactly the reference's init -> phase 1 -> phase 3 (tiles in order) ->
-// phase 2, so with Math::exact H is bit-identical to update_h_tiled.
-constexpr int kLThreads = 512;
-constexpr int kLQuad = 4;  // columns per update thread (independent chains)
-
-struct LookArgs {
-    int64_t n;
-    int k;
-    int tile;
-    double eps;
-    int use_diag;
-    int rows_per_cta;
-    const double* old_m;   // n x k
-    double* out;           // n x k, the updated factor
-    const double* coeff;   // k x k
-    const double* add;     // n x k
-    double* norms;         // k            (normalize)
-    double* partials;      // k x gridDim  (normalize)
-    unsigned* counters;    // k, zeroed    (normalize)
-    double* totals;        // k, NaN       (normalize)
-    long long* prof;       // optional per-CTA section cycles (PLNMF_PROFILE=1)
-    int overlap;           // 1: look-ahead concurrent with the chain; 0: at the tile boundary
-    unsigned long long* trace;  // debug: exchange timestamps (k x grid x 3)
-    const double* qpanel;  // [tile][k][TQ] column panels of coeff (zero-padded), built per update
-    int stage_ops;         // 1: the tile's old/add operands are staged in shared memory
-    int sqn_smem;          // 1: the next tile's coeff panel is staged in shared memory
-};
-
-enum { kProfPro = 0, kProfChain = 1, kProfGrid = 2, kProfWait = 3, kProfBoundary = 4, kProfUpd = 5 };
-
-// acc(r, c) += sum over kk in [k0, k1) of -coeff(kk, c) * src(r, kk), for the
-// kLQuad columns c0.. (c < cend); src row pointer srow (global or shared).
-template <class M>
-__device__ __forceinline__ void accumulate_quad(double (&acc)[kLQuad], const double* srow, int k0, int k1,
-                                                const double* sq, int ldq, int cq, int wq) {
-#pragma unroll 4
-    for (int kk = k0; kk < k1; ++kk) {
-        const double x = srow[kk];
-        const double* q = sq + kk * ldq + cq;
-#pragma unroll
-        for (int u = 0; u < kLQuad; ++u)
-            if (u < wq) acc[u] = M::madd(acc[u], -1.0 * q[u], x);
-    }
-}
-
-// acc[u] += -coeff(kk, c0+u) * src[kk] for kk in [k0, k1), u < C (coefficient
-// row kk of the next tile's columns at sq + kk*ldq + c0, 16-byte aligned).
-// Columns past the tile width have zero coefficients in sq, so they stay 0.
-template <class M, int C>
-__device__ __forceinline__ void row_panel(double (&acc)[C], const double* __restrict__ src, int k0, int k1,
-                                          const double* sq, int ldq, int c0) {
-#pragma unroll 4
-    for (int kk = k0; kk < k1; ++kk) {
-        const double x = src[kk];
-        const double2* q2 = reinterpret_cast<const double2*>(sq + kk * ldq + c0);
-#pragma unroll
-        for (int u = 0; u < C / 2; ++u) {
-            const double2 qq = q2[u];
-            acc[2 * u] = M::madd(acc[2 * u], -1.0 * qq.x, x);
-            acc[2 * u + 1] = M::madd(acc[2 * u + 1], -1.0 * qq.y, x);
-        }
-    }
-}
-
-// TMAX > 0: the chain thread keeps its row of the current tile in registers
-// (x[j] = old value, replaced by the finished value once column j is done —
-// exactly the operand the reference reads: new for j < t, old for j >= t), so
-// each column's scratch sum is a pure register DADD chain.  TMAX = 0: generic
-// shared-memory path for tiles wider than 32.
-template <class M, bool NORMALIZE, int TMAX, bool STAGE, bool SQN>
-__global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
-    extern __shared__ double smem[];
-    const int T = p.tile, k = p.k, ldt = T + 1;
-    const int TQ = (T + 7) & ~7;  // sqn leading dimension: whole 8-column panels, 16-byte rows
-    const int R = p.rows_per_cta;
-    const int64_t r0 = (int64_t)blockIdx.x * R;
-    const int nrows = (int)((r0 + R < p.n) ? R : (p.n > r0 ? p.n - r0 : 0));
-    const int tid = threadIdx.x;
-    // The chain warps take the HIGHEST warp ids: the issue arbiter favours
-    // high warp ids, and the chain is the latency-critical path while the
-    // look-ahead warps saturate the fp64 pipes.
-    // Chain = row warps (one row per thread) + for W one exchange warp that
-    // runs the grid exchange while the row warps precompute the next column's
-    // prefix terms.
-    const int row_warps = min(8, max(1, (R + kWarp - 1) / kWarp));
-    const int nrowt = row_warps * kWarp;
-    const int chain_warps = row_warps + (NORMALIZE ? 1 : 0);
-    const int nchain = chain_warps * kWarp;
-    const int nupd = kLThreads - nchain;
-    const bool is_chain = tid >= nupd;
-    const int ctid = tid - nupd;  // chain-local thread id
-    const bool is_xwarp = NORMALIZE && ctid >= nrowt;
-    const int utid = tid;         // look-ahead thread id
-
-    // double-buffered per-tile blocks: accumulators and (optionally) the old
-    // values / additive term; optionally the next tile's coeff panel.  Shapes
-    // too large for shared memory read those from global (L1) instead.
-    const int64_t blk = (int64_t)R * ldt;
-    double* acc[2] = {smem, smem + blk};
-    double* oldB[2] = {smem + 2 * blk, smem + 3 * blk};
-    double* addB[2] = {smem + 4 * blk, smem + 5 * blk};
-    double* sqn = smem + (STAGE ? 6 : 2) * blk;  // k x TQ: coeff(:, next tile's columns), zero-padded
-    double* sqc = sqn + (SQN ? (int64_t)k * TQ : 0);  // T x T: coeff(tile, tile) of the current tile
-    double* red = sqc + (int64_t)T * T;                // 48
-
-    // Section timers stay in registers (no memory traffic on the critical
-    // path) and are written once at the end; look-ahead warp 0 records the
-    // prologue / wait / look-ahead / boundary sections, chain warp 0 the chain,
-    // grid-exchange and chain-side wait sections.
-    long long t0 = clock64();
-    long long sec_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    auto mark = [&](int sec) {
-        if (p.prof) {
-            const long long now = clock64();
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (i == sec) sec_t[i] += now - t0;
-            t0 = now;
-        }
-    };
-
-    // the coeff panel of the tile starting at column bn: shared copy or global panel
-    auto Qn = [&](int bn) -> const double* {
-        return SQN ? sqn : p.qpanel + (int64_t)(bn / T) * k * TQ;
-    };
-    // Builds the accumulators of the tile [bn, en) except the phase-3 term of
-    // the tile just before it: init + phase 1 + phase 3 from [0, b_prev).
-    // Run by `count` threads, this one being number `self`.
-    // Register-tile path (TMAX > 0): a thread owns 8 consecutive columns of one
-    // row (8 independent chains); one load of the row operand feeds 8 MACs and
-    // the 8 coefficients come as 4 vector LDS.128 from sqn (ld TQ, even).
-    auto build_next = [&](double* dst, int bn, int en, int bprev, int first, int count, int self) {
-        const double* Q = Qn(bn);
-        if (TMAX > 0) {
-            constexpr int C8 = 8;
-            const int wn = en - bn;
-            const int ng = (wn + C8 - 1) / C8;
-            for (int item = self; item < nrows * ng; item += count) {
-                const int r = item / ng, cq = (item % ng) * C8;
-                const int64_t g = (r0 + r) * k;
-                double a[C8];
-#pragma unroll
-                for (int u = 0; u < C8; ++u) {
-                    a[u] = 0.0;
-                    if (cq + u < wn) {
-                        const int c = bn + cq + u;
-                        const double o = p.old_m[g + c];
-                        a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
-                    }
-                }
-                row_panel<M, C8>(a, p.old_m + g, en, k, Q, TQ, cq);   // phase 1
-                row_panel<M, C8>(a, p.out + g, 0, bprev, Q, TQ, cq);  // phase 3, tiles before the previous
-#pragma unroll
-                for (int u = 0; u < C8; ++u)
-                    if (cq + u < wn) dst[r * ldt + cq + u] = a[u];
-            }
-            return;
-        }
-        const int wn = en - bn;
-        const int nq = (wn + kLQuad - 1) / kLQuad;
-        for (int item = self; item < nrows * nq; item += count) {
-            const int r = item / nq, cq = (item % nq) * kLQuad;
-            const int wq = min(kLQuad, wn - cq);
-            const int64_t g = (r0 + r) * k;
-            double a[kLQuad];
-#pragma unroll
-            for (int u = 0; u < kLQuad; ++u) {
-                a[u] = 0.0;
-                if (u < wq) {
-                    const int c = bn + cq + u;
-                    const double o = p.old_m[g + c];
-                    a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
-                }
-            }
-            accumulate_quad<M>(a, p.old_m + g, en, k, Q, TQ, cq, wq);  // phase 1
-            accumulate_quad<M>(a, p.out + g, 0, bprev, Q, TQ, cq, wq);  // phase 3, tiles before the previous
-#pragma unroll
-            for (int u = 0; u < kLQuad; ++u)
-                if (u < wq) dst[r * ldt + cq + u] = a[u];
-        }
-        (void)first;
-    };
-    auto load_sqn = [&](int bn, int en, int self, int count) {
-        (void)en;
-        if (!SQN) return;
-        const double* src = p.qpanel + (int64_t)(bn / T) * k * TQ;
-        for (int idx = self; idx < k * TQ; idx += count) sqn[idx] = src[idx];
-    };
-    auto load_sqc = [&](int b, int e, int self, int count) {
-        const int w = e - b;
-        for (int idx = self; idx < w * w; idx += count) {
-            const int i = idx / w, j = idx % w;
-            sqc[i * T + j] = p.coeff[(int64_t)(b + i) * k + b + j];
-        }
-    };
-
-    // old / additive values of the tile [bn, en) for this CTA's rows (coalesced rows of w doubles)
-    auto stage_tile = [&](int buf, int bn, int en, int self, int count) {
-        if (!STAGE) return;
-        const int wn = en - bn;
-        for (int idx = self; idx < nrows * wn; idx += count) {
-            const int r = idx / wn, j = idx % wn;
-            const int64_t g = (r0 + r) * k + bn + j;
-            oldB[buf][r * ldt + j] = p.old_m[g];
-            addB[buf][r * ldt + j] = p.add[g];
-        }
-    };
-
-    // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks, tile-0 operands
-    {
-        const int e0 = min(T, k);
-        load_sqn(0, e0, tid, kLThreads);
-        load_sqc(0, e0, tid, kLThreads);
-        stage_tile(0, 0, e0, tid, kLThreads);
-        __syncthreads();
-        build_next(acc[0], 0, e0, 0, 0, kLThreads, tid);
-        __syncthreads();
-    }
-    mark(kProfPro);
-
-    int cur = 0;
-    for (int b = 0; b < k; b += T) {
-        const int e = min(b + T, k), w = e - b;
-        const int bn = e, en = min(e + T, k);
-        const bool has_next = bn < k;
-        double* A = acc[cur];
-        if (is_chain && TMAX > 0) {
-            // ---- phase 2 of this tile, register-resident rows (one row per row thread)
-            constexpr int TM = TMAX > 0 ? TMAX : 1;
-            const int r = ctid;
-            const bool own = !is_xwarp && r < nrows;
-            double x[TM];
-            double* arow = A + r * ldt;
-            const double* addr = STAGE ? addB[cur] + r * ldt : p.add + (r0 + r) * k + b;
-            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
-#pragma unroll
-            for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
-            double pre = 0.0;  // sum_{j < tt-1} x[j] c(j, tt), precomputed during the previous exchange
-            double add_next = own ? addr[0] : 0.0;  // additive term, loaded one column ahead
-#pragma unroll
-            for (int tt = 0; tt < TM; ++tt) {
-                if (tt < w) {
-                    double val = 0.0;
-                    const double add_t = add_next;
-                    if (own && tt + 1 < w) add_next = addr[tt + 1];  // in flight across this column's exchange
-                    if (own) {
-                        const double a_t = arow[tt];
-                        double s = NORMALIZE ? pre : 0.0;
-#pragma unroll
-                        for (int j = 0; j < TM; ++j) {
-                            // scratch terms in the reference's order: new (j < tt), then old (j >= tt)
-                            const bool take = NORMALIZE ? (j + 1 >= tt && j < w) : (j < w);
-                            if (take) s = M::madd(s, x[j], sqc[j * T + tt]);
-                        }
-                        val = clamp_floor(p.eps, dsub(dadd(a_t, add_t), s));
-                    }
-                    if (NORMALIZE) {
-                        if (!is_xwarp) {
-                            const double ss = warp_sum_lane0(M::madd(0.0, val, val));
-                            if (lane_id() == 0) red[ctid >> 5] = ss;
-                        }
-                        named_sync(1, nchain);
-                        if (is_xwarp) {
-                            double blk = 0.0;
-                            if (lane_id() == 0) {
-                                blk = red[0];
-                                for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
-                            }
-                            blk = __shfl_sync(0xffffffffu, blk, 0);
-                            mark(kProfChain);
-                            const double norm =
-                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
-                            if (lane_id() == 0) {
-                                red[40] = norm;
-                                if (blockIdx.x == 0) p.norms[b + tt] = norm;
-                            }
-                            mark(kProfGrid);
-                        } else if (own && tt + 1 < w) {
-                            // next column's prefix: terms j < tt (all final) — overlaps the exchange
-                            pre = 0.0;
-#pragma unroll
-                            for (int j = 0; j < TM; ++j)
-                                if (j < tt) pre = M::madd(pre, x[j], sqc[j * T + tt + 1]);
-                        }
-                        named_sync(1, nchain);
-                        val = clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
-                    }
-                    x[tt] = val;
-                    if (own) arow[tt] = val;
-                }
-            }
-            named_sync(1, nchain);
-            for (int idx = ctid; idx < nrows * w; idx += nchain) {
-                const int rr = idx / w, j = idx % w;
-                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
-            }
-            mark(kProfChain);
-        } else if (is_chain) {
-            // ---- phase 2 of this tile (generic shared-memory path)
-            const double* oldT = STAGE ? oldB[cur] : p.old_m + r0 * k + b;
-            const double* addT = STAGE ? addB[cur] : p.add + r0 * k + b;
-            const int64_t ldo = STAGE ? ldt : k;
-            for (int t = b; t < e; ++t) {
-                const int tt = t - b;
-                double ss = 0.0;
-                for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
-                    double* nr = A + r * ldt;
-                    const double* orow = oldT + r * ldo;
-                    double s = 0.0;
-                    for (int j = 0; j < tt; ++j) s = M::madd(s, nr[j], sqc[j * T + tt]);
-                    for (int j = tt; j < w; ++j) s = M::madd(s, orow[j], sqc[j * T + tt]);
-                    const double val = clamp_floor(p.eps, dsub(dadd(nr[tt], addT[r * ldo + tt]), s));
-                    nr[tt] = val;
-                    if (NORMALIZE) ss = M::madd(ss, val, val);
-                }
-                if (NORMALIZE) {
-                    // chain-group reduction (fixed tree), then the grid exchange
-                    if (!is_xwarp) {
-                        ss = warp_sum_lane0(ss);
-                        if (lane_id() == 0) red[ctid >> 5] = ss;
-                    }
-                    named_sync(1, nchain);
-                    if (is_xwarp) {
-                        double blk = 0.0;
-                        if (lane_id() == 0) {
-                            blk = red[0];
-                            for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
-                        }
-                        blk = __shfl_sync(0xffffffffu, blk, 0);
-                        mark(kProfChain);
-                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters, p.trace);
-                        if (lane_id() == 0) {
-                            red[40] = norm;
-                            if (blockIdx.x == 0) p.norms[t] = norm;
-                        }
-                        mark(kProfGrid);
-                    }
-                    named_sync(1, nchain);
-                    const double norm = red[40];
-                    for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
-                        double* x = A + r * ldt + tt;
-                        *x = clamp_floor(p.eps, __ddiv_rn(*x, norm));  // tiled.cpp:146
-                    }
-                }
-            }
-            // publish the finished tile (rows were thread-private until here)
-            named_sync(1, nchain);
-            for (int idx = ctid; idx < nrows * w; idx += nchain) {
-                const int r = idx / w, j = idx % w;
-                p.out[(r0 + r) * k + b + j] = A[r * ldt + j];
-            }
-            mark(kProfChain);
-        } else if (has_next && p.overlap) {
-            // ---- look-ahead: next tile's accumulators, minus this tile's phase-3 term
-            load_sqn(bn, en, utid, nupd);
-            stage_tile(cur ^ 1, bn, en, utid, nupd);
-            named_sync(2, nupd);
-            build_next(acc[cur ^ 1], bn, en, b, 0, nupd, utid);
-            mark(kProfUpd);
-        }
-        __syncthreads();
-        mark(kProfWait);
-        if (has_next && !p.overlap) {
-            load_sqn(bn, en, tid, kLThreads);
-            stage_tile(cur ^ 1, bn, en, tid, kLThreads);
-            __syncthreads();
-            build_next(acc[cur ^ 1], bn, en, b, 0, kLThreads, tid);
-            __syncthreads();
-            mark(kProfUpd);
-        }
-        if (has_next) {
-            // ---- boundary: this tile's phase-3 term into the next tile, coeff block of the next tile
-            double* An = acc[cur ^ 1];
-            const int wn = en - bn, nq = (wn + kLQuad - 1) / kLQuad;
-            for (int item = tid; item < nrows * nq; item += kLThreads) {
-                const int r = item / nq, cq = (item % nq) * kLQuad;
-                const int wq = min(kLQuad, wn - cq);
-                double a[kLQuad];
-#pragma unroll
-                for (int u = 0; u < kLQuad; ++u) a[u] = (u < wq) ? An[r * ldt + cq + u] : 0.0;
-                // src row = finished tile values, indexed by absolute kk in [b, e)
-                accumulate_quad<M>(a, A + r * ldt - b, b, e, Qn(bn), TQ, cq, wq);
-#pragma unroll
-                for (int u = 0; u < kLQuad; ++u)
-                    if (u < wq) An[r * ldt + cq + u] = a[u];
-            }
-            load_sqc(bn, en, tid, kLThreads);
-            __syncthreads();
-            mark(kProfBoundary);
-        }
-        cur ^= 1;
-    }
-    if (p.prof && (tid == 0 || tid == nupd)) {
-        const int slot = (tid == 0) ? 0 : 8;  // look-ahead view, chain view
-#pragma unroll
-        for (int i = 0; i < 8; ++i) p.prof[blockIdx.x * 16 + slot + i] = sec_t[i];
-    }
-}
+using upd::LookArgs;
+using upd::launch_pl;
+using upd::kLThreads;
 
 int sm_count(int device) {
     int n = 0;
@@ -466,10 +60,12 @@ int sm_count(int device) {
     return n;
 }
 
-size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem) {
+size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem, int kc, int kst = 2,
+               bool normalize = false) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
-    return sizeof(double) * (size_t)((stage_ops ? 6 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
-                                     tile * tile + 48);
+    const int64_t prods = (normalize && tile <= 32) ? rows * tile : 0;  // W chain products (exact path)
+    return sizeof(double) * (size_t)((stage_ops ? 4 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
+                                     tile * tile + 48 + 1 + (kc > 0 ? kst * rows * (kc + 2) : 0) + prods);
 }
 
 // qpanel[tau][kk][j] = coeff(kk, b_tau + j) for j < width(tau), 0 up to TQ.
@@ -563,36 +159,6 @@ __global__ void __launch_bounds__(kRefWThreads) ref_update_w_kernel(RefWArgs a) 
     }
 }
 
-template <class M, bool NORM, int TMAX, bool STAGE, bool SQN>
-void launch_pl_t(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
-    auto fn = pl_update_kernel<M, NORM, TMAX, STAGE, SQN>;
-    PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
-    const dim3 grid((unsigned)plan.grid), block(kLThreads);
-    if (NORM) {
-        void* args[] = {&a};
-        PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, plan.smem, s));
-    } else {
-        fn<<<grid, block, plan.smem, s>>>(a);
-    }
-}
-
-// Shared-memory variants: both staged, panel only, neither (the planner
-// never picks "operands staged, panel global").
-template <class M, bool NORM, int TMAX>
-void launch_pl_s(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
-    if (plan.stage_ops) launch_pl_t<M, NORM, TMAX, true, true>(s, plan, a);
-    else if (plan.sqn_smem) launch_pl_t<M, NORM, TMAX, false, true>(s, plan, a);
-    else launch_pl_t<M, NORM, TMAX, false, false>(s, plan, a);
-}
-
-// Register-resident chains need one row per chain thread (<= 256 rows per CTA).
-template <class M, bool NORM>
-void launch_pl(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
-    const bool regs = plan.rows_per_cta <= 8 * kWarp;
-    if (regs && a.tile <= 16) launch_pl_s<M, NORM, 16>(s, plan, a);
-    else if (regs && a.tile <= 32) launch_pl_s<M, NORM, 32>(s, plan, a);
-    else launch_pl_s<M, NORM, 0>(s, plan, a);
-}
 
 }  // namespace
 
@@ -610,9 +176,13 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
     if (std::getenv("PLNMF_FORCE_STREAMING")) return plan_stream_update(n, k, tile, normalize, device);
     // shared-memory variants, most staged first
     const bool variants[3][2] = {{true, true}, {false, true}, {false, false}};
+    // the staged look-ahead GEMM wants >= 8-wide operand chunks; an unstaged
+    // look-ahead is the last resort of each variant
     auto pick = [&](int64_t rows) -> int {
         for (int v = 0; v < 3; ++v)
-            if (pl_smem(rows, k, tile, variants[v][0], variants[v][1]) <= (size_t)max_smem) return v;
+            if (pl_smem(rows, k, tile, variants[v][0], variants[v][1], kPrivKC, 2, normalize) <= (size_t)max_smem) return v;
+        for (int v = 0; v < 3; ++v)
+            if (pl_smem(rows, k, tile, variants[v][0], variants[v][1], 0, 2, normalize) <= (size_t)max_smem) return v;
         return -1;
     };
     int v = -1;
@@ -632,7 +202,22 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
     plan.stage_ops = variants[v][0];
     plan.sqn_smem = variants[v][1];
     plan.rows_per_cta = rpc;
-    plan.smem = pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem);
+    plan.kc = 0;
+    plan.kst = 0;
+    {
+        // the staged GEMM runs one item (row x 16 columns) per look-ahead thread
+        const int row_warps = (int)std::min<int64_t>(8, std::max<int64_t>(1, (rpc + 31) / 32));
+        const int nupd = kLThreads - 32 * (row_warps + (normalize ? 1 : 0));
+        const int64_t items = rpc * ((std::min<int64_t>(tile, k) + 15) / 16);
+        if (!std::getenv("PLNMF_NO_STAGED_GEMM") && plan.sqn_smem && items <= nupd)
+            for (int st : {3, 2})
+                if (pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, kPrivKC, st, normalize) <= (size_t)max_smem) {
+                    plan.kc = kPrivKC;
+                    plan.kst = st;
+                    break;
+                }
+    }
+    plan.smem = pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, plan.kc, plan.kst, normalize);
     return plan;
 }
 
@@ -650,8 +235,8 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
         return stream_update(s, m, plan, n, k, tile, eps, w_update, old_m, out, coeff, add, norms, partials,
                              counters);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
-               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : 1, nullptr,
-               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0};
+               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : std::getenv("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1, nullptr,
+               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst};
     {
         const int tq = (int)((tile + 7) & ~int64_t(7));
         qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(
@@ -660,8 +245,9 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     }
     static unsigned long long* trace_buf = nullptr;
     if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
-        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 3 * 1024 * 512));
+        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 11 * 1024 * 512));
         a.trace = trace_buf;
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 11 * 1024 * 512, s));
     }
     if (w_update) {
         exchange_reset(s, k, plan.grid, partials, counters);
@@ -674,31 +260,46 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     PLNMF_CUDA_CHECK(cudaGetLastError());
     if (a.trace) {
         const int g = plan.grid;
-        std::vector<unsigned long long> h((size_t)3 * k * g);
+        std::vector<unsigned long long> h((size_t)11 * k * g);
         PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
                                          cudaMemcpyDeviceToHost, s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
-        double skew = 0, poll = 0, read = 0, gap = 0;
-        for (int64_t t = 0; t < k; ++t) {
-            unsigned long long amin = ~0ull, amax = 0, cmin = ~0ull, cmax = 0, rmax = 0;
-            for (int c = 0; c < g; ++c) {
+        // SM-clock durations per CTA (clocks are per SM: only same-CTA differences are meaningful)
+        double poll = 0, read = 0, gap = 0, pmax = 0;
+        for (int c = 0; c < g; ++c) {
+            double cp = 0;
+            for (int64_t t = 0; t < k; ++t) {
                 const unsigned long long* x = &h[(size_t)(t * g + c) * 3];
-                amin = std::min(amin, x[0]); amax = std::max(amax, x[0]);
-                cmin = std::min(cmin, x[1]); cmax = std::max(cmax, x[1]);
-                rmax = std::max(rmax, x[2]);
+                cp += double(x[1] - x[0]);
+                read += double(x[2] - x[1]);
+                if (t > 0) gap += double(x[0] - h[(size_t)((t - 1) * g + c) * 3 + 2]);
             }
-            skew += double(amax - amin);
-            poll += double(cmax - amax);
-            read += double(rmax - cmax);
-            if (t > 0) {
-                unsigned long long pmax = 0;
-                for (int c = 0; c < g; ++c) pmax = std::max(pmax, h[(size_t)((t - 1) * g + c) * 3 + 2]);
-                gap += double(amin - pmax);
-            }
+            poll += cp;
+            pmax = std::max(pmax, cp / k);
         }
-        std::fprintf(stderr, "[plnmf] exchange trace (ns/column): arrival skew %.0f, last-arrival->all-complete %.0f, "
-                     "complete->partials read %.0f, prev-done->first-arrival %.0f\n",
-                     skew / k, poll / k, read / k, gap / (k - 1));
+        {
+            // chain stamps: [0] row warp released after the exchange, [1] next column's value ready,
+            // [2] its warp partial stored, [3] exchange warp past the reduction barrier, [4] norm published
+            const unsigned long long* c8 = h.data() + (size_t)3 * k * g;
+            double d01 = 0, d12 = 0, d23 = 0, d34 = 0, d40 = 0;
+            int n = 0;
+            for (int64_t t = 0; t + 1 < k; ++t)
+                for (int c = 0; c < g; ++c) {
+                    const unsigned long long* x = c8 + ((size_t)t * g + c) * 8;
+                    const unsigned long long* y = c8 + ((size_t)(t + 1) * g + c) * 8;
+                    if (!x[0] || !x[1] || !y[2] || !y[3] || !y[4]) continue;
+                    d01 += double(x[1] - x[0]); d12 += double(y[2] - x[1]); d23 += double(y[3] - y[2]);
+                    d34 += double(y[4] - y[3]); d40 += double(y[0] - y[4]);
+                    ++n;
+                }
+            if (n)
+                std::fprintf(stderr, "[plnmf] chain stamps (SM cycles): div+next value %.0f, warp reduce %.0f, "
+                             "barrier->exchange warp %.0f, exchange(+partial sum) %.0f, norm->row release %.0f\n",
+                             d01 / n, d12 / n, d23 / n, d34 / n, d40 / n);
+        }
+        std::fprintf(stderr, "[plnmf] exchange trace (SM cycles/column, mean over CTAs): arrival->complete %.0f "
+                     "(max CTA %.0f), complete->partials read %.0f, read->next arrival %.0f\n",
+                     poll / k / g, pmax, read / k / g, gap / (k - 1) / g);
     }
     return 1;
 }
@@ -744,3 +345,4 @@ int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v
 
 }  // namespace kern
 }  // namespace plnmf
+

@@ -1,0 +1,616 @@
+// The look-ahead tiled-update kernel template (pl_update_kernel) and its
+// launchers.  Instantiated per (Math, normalize) in update_inst_*.cu so the
+// four heavy instantiation sets compile in parallel; update.cu holds the host
+// side (planning, dispatch) and the reference (fast-hals) updaters.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "exchange.cuh"
+#include "kernels.cuh"
+#include "lookahead.cuh"
+
+namespace plnmf {
+namespace upd {
+
+
+
+// ---------------------------------------------------------------- look-ahead tiled update
+// One persistent kernel per factor update (W: cooperative, one CTA per SM, one
+// grid exchange per column; H: ordinary launch).  A CTA owns R consecutive
+// rows.  Its warps split into
+//   chain warps  (one thread per row): phase 2 of tile s, column by column —
+//                the latency-critical recurrence;
+//   update warps : meanwhile build tile s+1's accumulators
+//                  acc(r,c) = init(old(r,c)[*coeff(c,c)])           tiled.cpp:44
+//                           + sum_{kk >= e_{s+1}} -coeff(kk,c)*old(r,kk)   phase 1, :58-60
+//                           + sum_{kk <  b_s}     -coeff(kk,c)*out(r,kk)   phase 3 of tiles < s
+//                  — each term in the reference's order (kk ascending).
+// At the tile boundary all warps add tile s's phase-3 term to tile s+1 and
+// the next tile starts.  Finished tiles are written to `out` (global) where
+// later tiles' update warps read them.  The per-element operation sequence is
+// exactly the reference's init -> phase 1 -> phase 3 (tiles in order) ->
+// phase 2, so with Math::exact H is bit-identical to update_h_tiled.
+constexpr int kLThreads = 512;
+constexpr int kLQuad = 4;  // columns per update thread (independent chains)
+
+struct LookArgs {
+    int64_t n;
+    int k;
+    int tile;
+    double eps;
+    int use_diag;
+    int rows_per_cta;
+    const double* old_m;   // n x k
+    double* out;           // n x k, the updated factor
+    const double* coeff;   // k x k
+    const double* add;     // n x k
+    double* norms;         // k            (normalize)
+    double* partials;      // k x gridDim  (normalize)
+    unsigned* counters;    // k, zeroed    (normalize)
+    double* totals;        // k, NaN       (normalize)
+    long long* prof;       // optional per-CTA section cycles (PLNMF_PROFILE=1)
+    int overlap;           // 1: look-ahead concurrent with the chain; 0: at the tile boundary
+    unsigned long long* trace;  // debug: exchange timestamps (k x grid x 3)
+    const double* qpanel;  // [tile][k][TQ] column panels of coeff (zero-padded), built per update
+    int stage_ops;         // 1: the tile's old/add operands are staged in shared memory
+    int sqn_smem;          // 1: the next tile's coeff panel is staged in shared memory
+    int kc;                // >0: look-ahead operands staged in kc-wide chunks (lookahead_gemm_private)
+    int kst;               // ring depth of those chunks
+};
+
+template <class M>
+constexpr bool kExactM = false;
+template <>
+constexpr bool kExactM<MathExact> = true;
+
+enum { kProfPro = 0, kProfChain = 1, kProfGrid = 2, kProfWait = 3, kProfBoundary = 4, kProfUpd = 5, kProfDiv = 6,
+       kProfDot = 7 };
+
+// acc(r, c) += sum over kk in [k0, k1) of -coeff(kk, c) * src(r, kk), for the
+// kLQuad columns c0.. (c < cend); src row pointer srow (global or shared).
+template <class M>
+__device__ __forceinline__ void accumulate_quad(double (&acc)[kLQuad], const double* srow, int k0, int k1,
+                                                const double* sq, int ldq, int cq, int wq) {
+#pragma unroll 4
+    for (int kk = k0; kk < k1; ++kk) {
+        const double x = srow[kk];
+        const double* q = sq + kk * ldq + cq;
+#pragma unroll
+        for (int u = 0; u < kLQuad; ++u)
+            if (u < wq) acc[u] = M::madd(acc[u], -1.0 * q[u], x);
+    }
+}
+
+// acc[u] += -coeff(kk, c0+u) * src[kk] for kk in [k0, k1), u < C (coefficient
+// row kk of the next tile's columns at sq + kk*ldq + c0, 16-byte aligned).
+// Columns past the tile width have zero coefficients in sq, so they stay 0.
+template <class M, int C>
+__device__ __forceinline__ void row_panel(double (&acc)[C], const double* __restrict__ src, int k0, int k1,
+                                          const double* sq, int ldq, int c0) {
+#pragma unroll 4
+    for (int kk = k0; kk < k1; ++kk) {
+        const double x = src[kk];
+        const double2* q2 = reinterpret_cast<const double2*>(sq + kk * ldq + c0);
+#pragma unroll
+        for (int u = 0; u < C / 2; ++u) {
+            const double2 qq = q2[u];
+            acc[2 * u] = M::madd(acc[2 * u], -1.0 * qq.x, x);
+            acc[2 * u + 1] = M::madd(acc[2 * u + 1], -1.0 * qq.y, x);
+        }
+    }
+}
+
+// TMAX > 0: the chain thread keeps its row of the current tile in registers
+// (x[j] = old value, replaced by the finished value once column j is done —
+// exactly the operand the reference reads: new for j < t, old for j >= t), so
+// each column's scratch sum is a pure register DADD chain.  TMAX = 0: generic
+// shared-memory path for tiles wider than 32.
+template <class M, bool NORMALIZE, int TMAX, bool STAGE, bool SQN>
+__global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
+    extern __shared__ double smem[];
+    const int T = p.tile, k = p.k, ldt = T + 1;
+    const int TQ = (T + 7) & ~7;  // sqn leading dimension: whole 8-column panels, 16-byte rows
+    const int R = p.rows_per_cta;
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int nrows = (int)((r0 + R < p.n) ? R : (p.n > r0 ? p.n - r0 : 0));
+    const int tid = threadIdx.x;
+    // The chain warps take the HIGHEST warp ids: the issue arbiter favours
+    // high warp ids, and the chain is the latency-critical path while the
+    // look-ahead warps saturate the fp64 pipes.
+    // Chain = row warps (one row per thread) + for W one exchange warp that
+    // runs the grid exchange while the row warps precompute the next column's
+    // prefix terms.
+    const int row_warps = min(8, max(1, (R + kWarp - 1) / kWarp));
+    const int nrowt = row_warps * kWarp;
+    const int chain_warps = row_warps + (NORMALIZE ? 1 : 0);
+    const int nchain = chain_warps * kWarp;
+    const int nupd = kLThreads - nchain;
+    const bool is_chain = tid >= nupd;
+    const int ctid = tid - nupd;  // chain-local thread id
+    const bool is_xwarp = NORMALIZE && ctid >= nrowt;
+    const int utid = tid;         // look-ahead thread id
+
+    // double-buffered per-tile blocks: accumulators and (optionally) the old
+    // values / additive term; optionally the next tile's coeff panel.  Shapes
+    // too large for shared memory read those from global (L1) instead.
+    const int64_t blk = (int64_t)R * ldt;
+    double* acc[2] = {smem, smem + blk};
+    double* oldB[2] = {smem + 2 * blk, smem + 3 * blk};
+    double* sqn = smem + (STAGE ? 4 : 2) * blk;  // k x TQ: coeff(:, next tile's columns), zero-padded
+    double* sqc = sqn + (SQN ? (int64_t)k * TQ : 0);  // T x T: coeff(tile, tile) of the current tile
+    double* red = sqc + (int64_t)T * T;                // 48
+    // look-ahead GEMM operand chunks: p.kst buffers of R x (p.kc + 2), 16-byte aligned
+    double* xbuf0 = smem + ((((red + 48) - smem) + 1) & ~(int64_t)1);
+    // W chain (exact): per-row products of the next column's old terms, [j][row]
+    double* prodS = xbuf0 + (p.kc > 0 ? (int64_t)p.kst * R * (p.kc + 2) : 0);
+
+    // Profiled threads (look-ahead warp 0, chain warp 0, the exchange warp)
+    // add section durations straight to global (profiling runs only); no
+    // per-section registers in production.
+    long long* const prof_row =
+        p.prof ? ((tid == 0) ? p.prof + blockIdx.x * 24
+                  : (tid == nupd) ? p.prof + blockIdx.x * 24 + 8
+                  : (is_xwarp && ctid == nrowt) ? p.prof + blockIdx.x * 24 + 16 : nullptr)
+               : nullptr;
+    long long t0 = prof_row ? clock64() : 0;
+    auto mark = [&](int sec) {
+        if (prof_row) {
+            const long long now = clock64();
+            prof_row[sec] += now - t0;
+            t0 = now;
+        }
+    };
+
+    // the coeff panel of the tile starting at column bn: shared copy or global panel
+    auto Qn = [&](int bn) -> const double* {
+        return SQN ? sqn : p.qpanel + (int64_t)(bn / T) * k * TQ;
+    };
+    // Builds the accumulators of the tile [bn, en) except the phase-3 term of
+    // the tile just before it: init + phase 1 + phase 3 from [0, b_prev).
+    // Run by `count` threads, this one being number `self`.
+    // Register-tile path (TMAX > 0): a thread owns 8 consecutive columns of one
+    // row (8 independent chains); one load of the row operand feeds 8 MACs and
+    // the 8 coefficients come as 4 vector LDS.128 from sqn (ld TQ, even).
+    // Staged look-ahead GEMM (p.kc > 0, SQN, run by the look-ahead group):
+    // lookahead_gemm_private, one row x 16 columns per thread, each thread
+    // streaming its own row's operands through a p.kst-deep cp.async ring.
+    auto gemm_next = [&](double* dst, int bn, int en, int bprev, int count, int self) {
+        GemmArgs ga{dst, ldt, Qn(bn), TQ, bn, en, bprev, p.use_diag, p.old_m, p.out, r0, nrows, k, xbuf0,
+                    R * (kPrivKC + 2), count, self, 2};
+        if (TQ == 16) {
+            if (p.kst >= 3) lookahead_gemm_private<M, 16, kPrivKC, 3, 16>(ga);
+            else lookahead_gemm_private<M, 16, kPrivKC, 2, 16>(ga);
+        } else {
+            if (p.kst >= 3) lookahead_gemm_private<M, 16, kPrivKC, 3>(ga);
+            else lookahead_gemm_private<M, 16, kPrivKC, 2>(ga);
+        }
+    };
+    auto build_next = [&](double* dst, int bn, int en, int bprev, int first, int count, int self) {
+        const double* Q = Qn(bn);
+        if (TMAX > 0 && SQN && p.kc > 0 && count == nupd) {
+            gemm_next(dst, bn, en, bprev, count, self);
+            return;
+        }
+        if (TMAX > 0) {
+            constexpr int C8 = 8;
+            const int wn = en - bn;
+            const int ng = (wn + C8 - 1) / C8;
+            for (int item = self; item < nrows * ng; item += count) {
+                const int r = item / ng, cq = (item % ng) * C8;
+                const int64_t g = (r0 + r) * k;
+                double a[C8];
+#pragma unroll
+                for (int u = 0; u < C8; ++u) {
+                    a[u] = 0.0;
+                    if (cq + u < wn) {
+                        const int c = bn + cq + u;
+                        const double o = p.old_m[g + c];
+                        a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
+                    }
+                }
+                row_panel<M, C8>(a, p.old_m + g, en, k, Q, TQ, cq);   // phase 1
+                row_panel<M, C8>(a, p.out + g, 0, bprev, Q, TQ, cq);  // phase 3, tiles before the previous
+#pragma unroll
+                for (int u = 0; u < C8; ++u)
+                    if (cq + u < wn) dst[r * ldt + cq + u] = a[u];
+            }
+            return;
+        }
+        const int wn = en - bn;
+        const int nq = (wn + kLQuad - 1) / kLQuad;
+        for (int item = self; item < nrows * nq; item += count) {
+            const int r = item / nq, cq = (item % nq) * kLQuad;
+            const int wq = min(kLQuad, wn - cq);
+            const int64_t g = (r0 + r) * k;
+            double a[kLQuad];
+#pragma unroll
+            for (int u = 0; u < kLQuad; ++u) {
+                a[u] = 0.0;
+                if (u < wq) {
+                    const int c = bn + cq + u;
+                    const double o = p.old_m[g + c];
+                    a[u] = p.use_diag ? dmul(o, Q[c * TQ + cq + u]) : o;
+                }
+            }
+            accumulate_quad<M>(a, p.old_m + g, en, k, Q, TQ, cq, wq);  // phase 1
+            accumulate_quad<M>(a, p.out + g, 0, bprev, Q, TQ, cq, wq);  // phase 3, tiles before the previous
+#pragma unroll
+            for (int u = 0; u < kLQuad; ++u)
+                if (u < wq) dst[r * ldt + cq + u] = a[u];
+        }
+        (void)first;
+    };
+    auto load_sqn = [&](int bn, int en, int self, int count) {
+        (void)en;
+        if (!SQN) return;
+        const double* src = p.qpanel + (int64_t)(bn / T) * k * TQ;
+        // panel rows are whole 8-column groups: 16-byte cp.async, completed by
+        // the caller's cp_async_wait before its barrier
+        for (int idx = self; idx < k * TQ / 2; idx += count) cp_async16(sqn + 2 * idx, src + 2 * idx);
+        cp_async_commit();
+    };
+    auto load_sqc = [&](int b, int e, int self, int count) {
+        const int w = e - b;
+        for (int idx = self; idx < w * w; idx += count) {
+            const int i = idx / w, j = idx % w;
+            sqc[i * T + j] = p.coeff[(int64_t)(b + i) * k + b + j];
+        }
+    };
+
+    // old values of the tile [bn, en) for this CTA's rows (coalesced rows of w doubles); the
+    // additive term is read from global by the chain, one column ahead
+    auto stage_tile = [&](int buf, int bn, int en, int self, int count) {
+        if (!STAGE) return;
+        const int wn = en - bn;
+        for (int idx = self; idx < nrows * wn; idx += count) {
+            const int r = idx / wn, j = idx % wn;
+            const int64_t g = (r0 + r) * k + bn + j;
+            cp_async8(oldB[buf] + r * ldt + j, p.old_m + g);
+        }
+        cp_async_commit();
+    };
+
+    // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks, tile-0 operands
+    {
+        const int e0 = min(T, k);
+        load_sqn(0, e0, tid, kLThreads);
+        load_sqc(0, e0, tid, kLThreads);
+        stage_tile(0, 0, e0, tid, kLThreads);
+        cp_async_wait<0>();
+        __syncthreads();
+        if (p.kc > 0) {
+            if (!is_chain) build_next(acc[0], 0, e0, 0, 0, nupd, utid);
+        } else {
+            build_next(acc[0], 0, e0, 0, 0, kLThreads, tid);
+        }
+        __syncthreads();
+    }
+    mark(kProfPro);
+
+    int cur = 0;
+    double add_carry = 0.0;  // chain: the next tile's first additive term, prefetched
+    for (int b = 0; b < k; b += T) {
+        const int e = min(b + T, k), w = e - b;
+        const int bn = e, en = min(e + T, k);
+        const bool has_next = bn < k;
+        double* A = acc[cur];
+        if (is_chain && TMAX > 0 && NORMALIZE && kExactM<M>) {
+            // ---- W phase 2, latency-ordered (Math::exact).  Everything that does
+            // not depend on the column's norm is computed while the exchange is
+            // in flight: the next column's new-value prefix (pre), the products
+            // of its old-value terms (prod[j] = old_j * c(j, t+1): exact
+            // multiplications, the same bits the reference adds), its diagonal
+            // coefficient and a + add.  After the norm arrives only
+            //   div -> clamp -> mul -> add -> (w-t-1 dependent adds) -> sub -> clamp -> square
+            // remain before the next reduction: the reference's exact order.
+            // Operands stay in shared memory (old values: orow; finished values:
+            // arow, which the reference reads as `new`; the products: prodS).
+            constexpr int TM = TMAX > 0 ? TMAX : 1;
+            const int r = ctid;
+            const bool own = !is_xwarp && r < nrows;
+            double* prod = prodS + r;  // prod[j * R]: this row's products, conflict-free across lanes
+            double* arow = A + r * ldt;
+            const double* addr = p.add + (r0 + r) * k + b;
+            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+            // column 0 of the tile: every scratch term is old (tiled.cpp:118-131)
+            double val = 0.0;
+            {
+                const double add0 = b == 0 ? (own ? addr[0] : 0.0) : add_carry;
+                if (own) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int j = 0; j < TM; ++j)
+                        if (j < w) s = dadd(s, dmul(orow[j], sqc[j * T]));
+                    val = clamp_floor(p.eps, dsub(dadd(arow[0], add0), s));
+                }
+            }
+            // not unrolled: one column's code (exchange included) stays resident
+            // in the instruction cache across the whole update
+#pragma unroll 1
+            for (int tt = 0; tt < w; ++tt) {
+                {
+                    const bool more = tt + 1 < w;
+                    double add1 = 0.0;
+                    if (own && more) add1 = addr[tt + 1];  // in flight across this column's exchange
+                    if (own && !more && has_next) add_carry = addr[w];  // next tile's first column
+                    if (!is_xwarp) {
+                        const double ss = warp_sum_lane0(dmul(val, val));
+                        if (lane_id() == 0) red[ctid >> 5] = ss;
+                    }
+                    unsigned long long* sp8 = p.trace ? p.trace + (size_t)3 * k * gridDim.x +
+                                                            ((size_t)(b + tt) * gridDim.x + blockIdx.x) * 8
+                                                      : nullptr;
+                    if (sp8 && ctid == 0) sp8[2] = clock64();
+                    mark(kProfDot);
+                    named_sync(1, nchain);
+                    if (sp8 && ctid == nrowt) sp8[3] = clock64();
+                    double pre = 0.0, c1 = 0.0, u1 = 0.0;
+                    if (is_xwarp) {
+                        double blk = 0.0;
+                        if (lane_id() == 0) {
+                            blk = red[0];
+                            for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+                        }
+                        blk = __shfl_sync(0xffffffffu, blk, 0);
+                        mark(kProfChain);
+                        const double norm = grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
+                        if (lane_id() == 0) {
+                            red[40] = norm;
+                            if (blockIdx.x == 0) p.norms[b + tt] = norm;
+                        }
+                        if (sp8 && lane_id() == 0) sp8[4] = clock64() + (unsigned long long)(norm * 0.0);
+                        mark(kProfGrid);
+                    } else if (own && more) {
+                        // next column's norm-independent parts, overlapping the exchange
+#pragma unroll
+                        for (int j = 0; j < TM; ++j)
+                            if (j < tt) pre = dadd(pre, dmul(arow[j], sqc[j * T + tt + 1]));
+#pragma unroll
+                        for (int j = 0; j < TM; ++j)
+                            if (j > tt && j < w) prod[j * R] = dmul(orow[j], sqc[j * T + tt + 1]);
+                        c1 = sqc[tt * T + tt + 1];
+                        u1 = dadd(arow[tt + 1], add1);
+                        mark(kProfUpd);
+                    }
+                    named_sync(1, nchain);
+                    unsigned long long* st8 = p.trace ? p.trace + (size_t)3 * k * gridDim.x +
+                                                            ((size_t)(b + tt) * gridDim.x + blockIdx.x) * 8
+                                                      : nullptr;
+                    const bool stamp = st8 && ctid == 0;
+                    if (stamp) st8[0] = clock64();
+                    const double nv = clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
+                    if (own) {
+                        arow[tt] = nv;
+                        if (more) {
+                            double s2 = dadd(pre, dmul(nv, c1));
+#pragma unroll
+                            for (int j = 0; j < TM; ++j)
+                                if (j > tt && j < w) s2 = dadd(s2, prod[j * R]);
+                            val = clamp_floor(p.eps, dsub(u1, s2));
+                        }
+                    }
+                    if (stamp) st8[1] = clock64() + (unsigned long long)(val * 0.0);
+                    mark(kProfDiv);
+                }
+            }
+            named_sync(1, nchain);
+            for (int idx = ctid; idx < nrows * w; idx += nchain) {
+                const int rr = idx / w, j = idx % w;
+                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+            }
+            mark(kProfChain);
+        } else if (is_chain && TMAX > 0) {
+            // ---- phase 2 of this tile, register-resident rows (one row per row thread)
+            constexpr int TM = TMAX > 0 ? TMAX : 1;
+            const int r = ctid;
+            const bool own = !is_xwarp && r < nrows;
+            double x[TM];
+            double* arow = A + r * ldt;
+            const double* addr = p.add + (r0 + r) * k + b;
+            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+#pragma unroll
+            for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
+            double pre = 0.0;  // sum_{j < tt-1} x[j] c(j, tt), precomputed during the previous exchange
+            double add_next = b == 0 ? (own ? addr[0] : 0.0) : add_carry;  // loaded one column ahead
+#pragma unroll
+            for (int tt = 0; tt < TM; ++tt) {
+                if (tt < w) {
+                    double val = 0.0;
+                    const double add_t = add_next;
+                    if (own && tt + 1 < w) add_next = addr[tt + 1];  // in flight across this column's exchange
+                    if (own && tt + 1 == w && has_next) add_carry = addr[w];  // next tile's first column
+                    if (own) {
+                        const double a_t = arow[tt];
+                        double s = NORMALIZE ? pre : 0.0;
+#pragma unroll
+                        for (int j = 0; j < TM; ++j) {
+                            // scratch terms in the reference's order: new (j < tt), then old (j >= tt)
+                            const bool take = NORMALIZE ? (j + 1 >= tt && j < w) : (j < w);
+                            if (take) s = M::madd(s, x[j], sqc[j * T + tt]);
+                        }
+                        val = clamp_floor(p.eps, dsub(dadd(a_t, add_t), s));
+                    }
+                    mark(kProfDot);
+                    if (NORMALIZE) {
+                        if (!is_xwarp) {
+                            const double ss = warp_sum_lane0(M::madd(0.0, val, val));
+                            if (lane_id() == 0) red[ctid >> 5] = ss;
+                        }
+                        mark(kProfChain);
+                        named_sync(1, nchain);
+                        mark(kProfWait);
+                        if (is_xwarp) {
+                            double blk = 0.0;
+                            if (lane_id() == 0) {
+                                blk = red[0];
+                                for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+                            }
+                            blk = __shfl_sync(0xffffffffu, blk, 0);
+                            mark(kProfChain);
+                            const double norm =
+                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
+                            if (lane_id() == 0) {
+                                red[40] = norm;
+                                if (blockIdx.x == 0) p.norms[b + tt] = norm;
+                            }
+                            mark(kProfGrid);
+                        } else if (own && tt + 1 < w) {
+                            // next column's prefix: terms j < tt (all final) — overlaps the exchange
+                            pre = 0.0;
+#pragma unroll
+                            for (int j = 0; j < TM; ++j)
+                                if (j < tt) pre = M::madd(pre, x[j], sqc[j * T + tt + 1]);
+                            mark(kProfUpd);
+                        }
+                        named_sync(1, nchain);
+                        mark(kProfWait);
+                        val = clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
+                    }
+                    x[tt] = val;
+                    if (own) arow[tt] = val;
+                    mark(kProfDiv);
+                }
+            }
+            named_sync(1, nchain);
+            for (int idx = ctid; idx < nrows * w; idx += nchain) {
+                const int rr = idx / w, j = idx % w;
+                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+            }
+            mark(kProfChain);
+        } else if (is_chain) {
+            // ---- phase 2 of this tile (generic shared-memory path)
+            const double* oldT = STAGE ? oldB[cur] : p.old_m + r0 * k + b;
+            const double* addT = p.add + r0 * k + b;
+            const int64_t ldo = STAGE ? ldt : k;
+            const int64_t lda = k;
+            for (int t = b; t < e; ++t) {
+                const int tt = t - b;
+                double ss = 0.0;
+                for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
+                    double* nr = A + r * ldt;
+                    const double* orow = oldT + r * ldo;
+                    double s = 0.0;
+                    for (int j = 0; j < tt; ++j) s = M::madd(s, nr[j], sqc[j * T + tt]);
+                    for (int j = tt; j < w; ++j) s = M::madd(s, orow[j], sqc[j * T + tt]);
+                    const double val = clamp_floor(p.eps, dsub(dadd(nr[tt], addT[r * lda + tt]), s));
+                    nr[tt] = val;
+                    if (NORMALIZE) ss = M::madd(ss, val, val);
+                }
+                if (NORMALIZE) {
+                    // chain-group reduction (fixed tree), then the grid exchange
+                    if (!is_xwarp) {
+                        ss = warp_sum_lane0(ss);
+                        if (lane_id() == 0) red[ctid >> 5] = ss;
+                    }
+                    named_sync(1, nchain);
+                    if (is_xwarp) {
+                        double blk = 0.0;
+                        if (lane_id() == 0) {
+                            blk = red[0];
+                            for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+                        }
+                        blk = __shfl_sync(0xffffffffu, blk, 0);
+                        mark(kProfChain);
+                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters, p.trace);
+                        if (lane_id() == 0) {
+                            red[40] = norm;
+                            if (blockIdx.x == 0) p.norms[t] = norm;
+                        }
+                        mark(kProfGrid);
+                    }
+                    named_sync(1, nchain);
+                    const double norm = red[40];
+                    for (int r = ctid; r < nrows && !is_xwarp; r += nrowt) {
+                        double* x = A + r * ldt + tt;
+                        *x = clamp_floor(p.eps, __ddiv_rn(*x, norm));  // tiled.cpp:146
+                    }
+                }
+            }
+            // publish the finished tile (rows were thread-private until here)
+            named_sync(1, nchain);
+            for (int idx = ctid; idx < nrows * w; idx += nchain) {
+                const int r = idx / w, j = idx % w;
+                p.out[(r0 + r) * k + b + j] = A[r * ldt + j];
+            }
+            mark(kProfChain);
+        } else if (has_next && p.overlap) {
+            // ---- look-ahead: next tile's accumulators, minus this tile's phase-3 term
+            load_sqn(bn, en, utid, nupd);
+            stage_tile(cur ^ 1, bn, en, utid, nupd);
+            cp_async_wait<0>();
+            named_sync(2, nupd);
+            if (p.overlap != 2) build_next(acc[cur ^ 1], bn, en, b, 0, nupd, utid);  // 2: timing probe only
+            mark(kProfUpd);
+        }
+        __syncthreads();
+        mark(kProfWait);
+        if (has_next && !p.overlap) {
+            load_sqn(bn, en, tid, kLThreads);
+            stage_tile(cur ^ 1, bn, en, tid, kLThreads);
+            cp_async_wait<0>();
+            __syncthreads();
+            build_next(acc[cur ^ 1], bn, en, b, 0, kLThreads, tid);
+            __syncthreads();
+            mark(kProfUpd);
+        }
+        if (has_next) {
+            // ---- boundary: this tile's phase-3 term into the next tile, coeff block of the next tile
+            double* An = acc[cur ^ 1];
+            const int wn = en - bn, nq = (wn + kLQuad - 1) / kLQuad;
+            for (int item = tid; item < nrows * nq; item += kLThreads) {
+                const int r = item / nq, cq = (item % nq) * kLQuad;
+                const int wq = min(kLQuad, wn - cq);
+                double a[kLQuad];
+#pragma unroll
+                for (int u = 0; u < kLQuad; ++u) a[u] = (u < wq) ? An[r * ldt + cq + u] : 0.0;
+                // src row = finished tile values, indexed by absolute kk in [b, e)
+                accumulate_quad<M>(a, A + r * ldt - b, b, e, Qn(bn), TQ, cq, wq);
+#pragma unroll
+                for (int u = 0; u < kLQuad; ++u)
+                    if (u < wq) An[r * ldt + cq + u] = a[u];
+            }
+            load_sqc(bn, en, tid, kLThreads);
+            __syncthreads();
+            mark(kProfBoundary);
+        }
+        cur ^= 1;
+    }
+}
+
+
+template <class M, bool NORM, int TMAX, bool STAGE, bool SQN>
+void launch_pl_t(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
+    auto fn = pl_update_kernel<M, NORM, TMAX, STAGE, SQN>;
+    PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+    const dim3 grid((unsigned)plan.grid), block(kLThreads);
+    if (NORM) {
+        void* args[] = {&a};
+        PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, plan.smem, s));
+    } else {
+        fn<<<grid, block, plan.smem, s>>>(a);
+    }
+}
+
+// Shared-memory variants: both staged, panel only, neither (the planner
+// never picks "operands staged, panel global").
+template <class M, bool NORM, int TMAX>
+void launch_pl_s(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
+    if (plan.stage_ops) launch_pl_t<M, NORM, TMAX, true, true>(s, plan, a);
+    else if (plan.sqn_smem) launch_pl_t<M, NORM, TMAX, false, true>(s, plan, a);
+    else launch_pl_t<M, NORM, TMAX, false, false>(s, plan, a);
+}
+
+// Register-resident chains need one row per chain thread (<= 256 rows per CTA).
+template <class M, bool NORM>
+void launch_pl(cudaStream_t s, const kern::PhaseBPlan& plan, LookArgs& a) {
+    const bool regs = plan.rows_per_cta <= 8 * kWarp;
+    if (regs && a.tile <= 16) launch_pl_s<M, NORM, 16>(s, plan, a);
+    else if (regs && a.tile <= 32) launch_pl_s<M, NORM, 32>(s, plan, a);
+    else launch_pl_s<M, NORM, 0>(s, plan, a);
+}
+
+
+}  // namespace upd
+}  // namespace plnmf
