@@ -936,6 +936,8 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
                     else e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
                     break;
                 case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch); break;
+                case 5: e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch); break;
+                case 6: precompute_w(e); break;  // Q = gram(Ht) || P = A Ht on two streams
                 case 3:  // successive W updates against the same P, Q (mutates W)
                     update_w(e, *cfg, cfg->tile_size > 0 ? PLNMF_ALGORITHM_TILED : PLNMF_ALGORITHM_REFERENCE);
                     break;

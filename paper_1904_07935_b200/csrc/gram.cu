@@ -43,7 +43,7 @@ __device__ __forceinline__ void decode_upper(int p, int ntile, int& ta, int& tb)
 // parallelism, half the registers); the combine kernel adds them as
 // (lane0 + 0.0) + lane1 exactly like the compiled reduction.
 template <class M>
-__global__ void __launch_bounds__(kGramThreads) gram_block_kernel(int64_t n, int k,
+__global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, int k,
                                                                   const double* __restrict__ m,
                                                                   double* __restrict__ part,
                                                                   int ntile) {

@@ -236,7 +236,8 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                              counters);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
                norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : std::getenv("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1, nullptr,
-               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst};
+               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst,
+               std::getenv("PLNMF_DBG") ? std::atoi(std::getenv("PLNMF_DBG")) : 0};
     {
         const int tq = (int)((tile + 7) & ~int64_t(7));
         qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(

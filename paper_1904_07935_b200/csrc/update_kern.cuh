@@ -58,6 +58,7 @@ struct LookArgs {
     int sqn_smem;          // 1: the next tile's coeff panel is staged in shared memory
     int kc;                // >0: look-ahead operands staged in kc-wide chunks (lookahead_gemm_private)
     int kst;               // ring depth of those chunks
+    int dbg;               // timing experiments only (PLNMF_DBG bitmask); 0 in production
 };
 
 template <class M>
@@ -332,11 +333,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             for (int tt = 0; tt < w; ++tt) {
                 {
                     const bool more = tt + 1 < w;
-                    double add1 = 0.0;
-                    if (own && more) add1 = addr[tt + 1];  // in flight across this column's exchange
-                    if (own && !more && has_next) add_carry = addr[w];  // next tile's first column
                     if (!is_xwarp) {
-                        const double ss = warp_sum_lane0(dmul(val, val));
+                        const double ss = (p.dbg & 8) ? val : warp_sum_lane0(dmul(val, val));
                         if (lane_id() == 0) red[ctid >> 5] = ss;
                     }
                     unsigned long long* sp8 = p.trace ? p.trace + (size_t)3 * k * gridDim.x +
@@ -362,7 +360,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         }
                         if (sp8 && lane_id() == 0) sp8[4] = clock64() + (unsigned long long)(norm * 0.0);
                         mark(kProfGrid);
-                    } else if (own && more) {
+                    } else if (own && !more && has_next) {
+                        add_carry = addr[w];  // next tile's first column
+                    } else if (own && more && !(p.dbg & 1)) {
                         // next column's norm-independent parts, overlapping the exchange
 #pragma unroll
                         for (int j = 0; j < TM; ++j)
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         for (int j = 0; j < TM; ++j)
                             if (j > tt && j < w) prod[j * R] = dmul(orow[j], sqc[j * T + tt + 1]);
                         c1 = sqc[tt * T + tt + 1];
-                        u1 = dadd(arow[tt + 1], add1);
+                        u1 = dadd(arow[tt + 1], addr[tt + 1]);  // L2 latency hidden by the exchange
                         mark(kProfUpd);
                     }
                     named_sync(1, nchain);
@@ -380,14 +380,16 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                                                       : nullptr;
                     const bool stamp = st8 && ctid == 0;
                     if (stamp) st8[0] = clock64();
-                    const double nv = clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
+                    const double nv = (p.dbg & 4) ? clamp_floor(p.eps, dmul(val, red[40]))
+                                                  : clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
                     if (own) {
                         arow[tt] = nv;
                         if (more) {
                             double s2 = dadd(pre, dmul(nv, c1));
+                            if (!(p.dbg & 2))
 #pragma unroll
-                            for (int j = 0; j < TM; ++j)
-                                if (j > tt && j < w) s2 = dadd(s2, prod[j * R]);
+                                for (int j = 0; j < TM; ++j)
+                                    if (j > tt && j < w) s2 = dadd(s2, prod[j * R]);
                             val = clamp_floor(p.eps, dsub(u1, s2));
                         }
                     }

@@ -27,12 +27,18 @@ __device__ __forceinline__ double wsum(double v) {
 constexpr int MAXL = 5;  // g <= 160
 constexpr int REP = 8;
 
+__device__ __forceinline__ double ldcg(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
 // read g NaN-sentinel slots (lane l: l, l+32, ...), fixed-order sum, all lanes get it
+template <bool WEAK = false>
 __device__ __forceinline__ double read_sum(const double* col, int g) {
     const int lane = threadIdx.x & 31;
     double v[MAXL];
 #pragma unroll
-    for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? ldr(col + lane + 32 * i) : 0.0;
+    for (int i = 0; i < MAXL; ++i) v[i] = (lane + 32 * i < g) ? (WEAK ? ldcg(col + lane + 32 * i) : ldr(col + lane + 32 * i)) : 0.0;
     for (;;) {
         bool pend = false;
 #pragma unroll
@@ -69,21 +75,30 @@ __global__ void xk(int ncol, double* slots, double* totals, unsigned* counters, 
         }
         const double blk = 1.0 + cta + t;
         double norm;
-        if (VAR == 0) {
+        if (VAR == 0 || VAR == 5 || VAR == 6) {
             double* base = slots + (size_t)t * REP * stride;
             unsigned* cb = counters + (size_t)t * REP * 64;
             if (lane < REP) {
                 str(base + lane * stride + cta, blk);
-                asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cb + lane * 64) : "memory");
+                if (VAR != 5) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cb + lane * 64) : "memory");
+                else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cb + lane * 64) : "memory");
             }
             const int rep = cta % REP;
             const long long c0 = clock64();
-            if (lane == 0)
-                while (ldru(cb + rep * 64) < (unsigned)g) {
+            if (lane == 0) {
+                if (VAR != 5) {
+                    while (ldru(cb + rep * 64) < (unsigned)g) {
+                    }
+                } else {
+                    unsigned v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cb + rep * 64) : "memory");
+                    } while (v < (unsigned)g);
                 }
+            }
             __syncwarp();
             const long long c1 = clock64();
-            norm = read_sum(base + rep * stride, g);
+            norm = VAR == 6 ? read_sum<true>(base + rep * stride, g) : read_sum(base + rep * stride, g);
             const long long c2 = clock64();
             p1 += c1 - c0;
             p2 += c2 - c1;
@@ -126,6 +141,10 @@ __global__ void xk(int ncol, double* slots, double* totals, unsigned* counters, 
                 if (isnan(v)) v = ldr(mine + lane);
             }
             norm = __shfl_sync(~0u, wsum(v), 0);
+        } else if (VAR == 4) {
+            // private mailboxes: CTA c's column-t box = slots[(t * g + c) * stride + sender]
+            for (int dst = lane; dst < g; dst += 32) str(slots + ((size_t)t * g + dst) * stride + cta, blk);
+            norm = read_sum(slots + ((size_t)t * g + cta) * stride, g);
         } else {
             constexpr int R3 = 16;
             double* base = slots + (size_t)t * R3 * stride;
@@ -140,10 +159,10 @@ __global__ void xk(int ncol, double* slots, double* totals, unsigned* counters, 
 int main(int argc, char** argv) {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int ncol = 240, g = sms;
+    const int ncol = 240, g = argc > 1 ? atoi(argv[1]) : sms;
     double *slots, *totals, *out;
     unsigned* counters;
-    const size_t nslots = (size_t)ncol * 16 * 192, ntot = (size_t)ncol * REP * 32;
+    const size_t nslots = (size_t)ncol * 160 * 192, ntot = (size_t)ncol * REP * 32;
     cudaMalloc(&slots, nslots * 8);
     cudaMalloc(&totals, ntot * 8);
     cudaMalloc(&out, sizeof(double) * g);
@@ -154,12 +173,12 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const char* names[] = {"counter + read partials (engine)", "reducer CTA + broadcast", "12-way group leaders",
-                           "all-poll, 16 replicas"};
-    void* fns[] = {(void*)xk<0>, (void*)xk<1>, (void*)xk<2>, (void*)xk<3>};
+                           "all-poll, 16 replicas", "private mailboxes", "counter release/acquire", "counter, weak .cg partial reads"};
+    void* fns[] = {(void*)xk<0>, (void*)xk<1>, (void*)xk<2>, (void*)xk<3>, (void*)xk<4>, (void*)xk<5>, (void*)xk<6>};
     for (int gap : {0, 1000}) {
         for (int jit : {0, 300}) {
             if (gap == 0 && jit) continue;
-            for (int v = 0; v < 4; ++v) {
+            for (int v = 0; v < 7; ++v) {
                 float best = 1e9;
                 for (int rep = 0; rep < 3; ++rep) {
                     cudaMemset(slots, 0xFF, nslots * 8);
@@ -181,7 +200,7 @@ int main(int argc, char** argv) {
                 for (int c = 0; c < g; ++c) { m1 += hp[2 * c]; m2 += hp[2 * c + 1]; }
                 printf("gap %4d jitter %3d  %-34s: %6.3f us/column (%s)", gap, jit, names[v], best * 1e3 / ncol,
                        cudaGetErrorString(cudaGetLastError()));
-                if (v == 0) printf("  poll %.0f cyc, read %.0f cyc per column", m1 / g / ncol, m2 / g / ncol);
+                if (v == 0 || v >= 5) printf("  poll %.0f cyc, read %.0f cyc per column", m1 / g / ncol, m2 / g / ncol);
                 printf("\n");
             }
         }

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(512, 1) bulk_kernel(int nrows_per, int64_t n, 
     if (threadIdx.x == 0) sink[blockIdx.x] = dst[0];
 }
 
-template <class M, int KC, int ST, int TQC = 0>
+template <class M, int KC, int ST, int TQC = 0, int CG = 16>
 __global__ void __launch_bounds__(512, 1) priv_kernel(int nrows_per, int64_t n, int k, int tile, const double* old_m,
                                                       const double* out, const double* qpanel, int nthreads,
                                                       double* sink) {
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(512, 1) priv_kernel(int nrows_per, int64_t n, 
         const int bn = b + tile, en = min(bn + tile, k);
         GemmArgs ga{dst, ldt, q, tq, bn, en, b, 1, old_m, out, r0, nrows, k, bufs, bufd, nthreads,
                     (int)threadIdx.x, 2};
-        lookahead_gemm_private<M, 16, KC, ST, TQC>(ga);
+        lookahead_gemm_private<M, CG, KC, ST, TQC>(ga);
     }
     named_sync(2, nthreads);
     if (threadIdx.x == 0) sink[blockIdx.x] = dst[0];
@@ -179,10 +179,9 @@ int main(int argc, char** argv) {
     };
     for (int nt : {288, 416}) {
         if (only_nt && nt != only_nt) continue;
-        run(priv_kernel<MathExact, 16, 2>, "private KC16 ST2", nt, false);
-        run(priv_kernel<MathExact, 16, 2, 16>, "private KC16 ST2 TQ16", nt, false);
-        run(priv_kernel<MathExact, 16, 3, 16>, "private KC16 ST3 TQ16", nt, false);
-        run(priv_kernel<MathFused, 16, 2, 16>, "private KC16 ST2 TQ16 fused", nt, true);
+        run(priv_kernel<MathExact, 16, 2, 16, 16>, "private CG16", nt, false);
+        run(priv_kernel<MathExact, 16, 2, 16, 8>, "private CG8", nt, false);
+        run(priv_kernel<MathExact, 16, 2, 16, 4>, "private CG4", nt, false);
     }
     return 0;
 }
