@@ -38,6 +38,7 @@ struct plnmf_gpu_engine {
     double *val = nullptr, *tval = nullptr, *a_dense = nullptr;
     double *w = nullptr, *ht = nullptr, *w_new = nullptr, *h_new = nullptr;
     double *p = nullptr, *q = nullptr, *r = nullptr, *sm = nullptr, *norms = nullptr;
+    double* r_next = nullptr;  // R of the current W computed ahead (iterate), swapped into r when used
     double *gram_scratch = nullptr, *partials = nullptr, *dot_partials = nullptr;
     double *scalars = nullptr;  // [0] pw, [1] sq, [2..4] error report, [5] direct sum
     double *staging = nullptr, *direct_partials = nullptr;
@@ -47,6 +48,8 @@ struct plnmf_gpu_engine {
     int64_t n_partials = 0, n_direct_partials = 0;
 
     bool s_valid = false;  // sm == gram(w) of the current w
+    bool r_valid = false;  // r == A^T w of the current w, computed ahead on s2 (iterate: join_r)
+    cudaEvent_t join_r = nullptr;
     uint64_t launches = 0, update_macs = 0;
     int64_t bytes = 0;
     int sms = 0;
@@ -95,6 +98,7 @@ void release(plnmf_gpu_engine* e) {
     if (e->host_scalars) cudaFreeHost(e->host_scalars);
     for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
     if (e->fork) cudaEventDestroy(e->fork);
+    if (e->join_r) cudaEventDestroy(e->join_r);
     if (e->join) cudaEventDestroy(e->join);
     if (e->s) cudaStreamDestroy(e->s);
     if (e->s2) cudaStreamDestroy(e->s2);
@@ -120,6 +124,7 @@ void setup_common(plnmf_gpu_engine* e, int device, int64_t rank) {
     PLNMF_CUDA_CHECK(cudaStreamCreateWithFlags(&e->s2, cudaStreamNonBlocking));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
+    PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join_r, cudaEventDisableTiming));
 }
 
 void alloc_workspace(plnmf_gpu_engine* e) {
@@ -130,6 +135,7 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     e->h_new = dalloc<double>(e, d * k);
     e->p = dalloc<double>(e, v * k);
     e->r = dalloc<double>(e, d * k);
+    e->r_next = dalloc<double>(e, d * k);
     e->q = dalloc<double>(e, k * k);
     e->sm = dalloc<double>(e, k * k);
     e->norms = dalloc<double>(e, k);
@@ -157,6 +163,15 @@ void alloc_workspace(plnmf_gpu_engine* e) {
 // kernel, same bits — the reference recomputes it, proj/src/solver.cpp:34 vs
 // proj/src/hals.cpp:31).
 void precompute_h(plnmf_gpu_engine* e) {
+    if (e->r_valid) {  // R was computed ahead, next to the last error evaluation
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join_r, 0));
+        std::swap(e->r, e->r_next);
+        e->r_valid = false;
+        if (e->s_valid) return;
+        e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+        e->s_valid = true;
+        return;
+    }
     const bool need_s = !e->s_valid;
     if (need_s) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
@@ -294,6 +309,7 @@ void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         e->update_macs += (uint64_t)e->v * e->k * (e->k + 3);
     }
     e->s_valid = false;
+    e->r_valid = false;
 }
 
 struct ErrorReport {
@@ -353,6 +369,7 @@ void set_factors(plnmf_gpu_engine* e, const double* w, const double* ht) {
     upload_factor(e, ht, e->d, e->ht);
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
     e->s_valid = false;
+    e->r_valid = false;
 }
 
 void get_factors(plnmf_gpu_engine* e, double* w, double* ht) {
@@ -438,6 +455,15 @@ void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, 
         }
         if (it % cfg.error_every == 0) {
             te = clock::now();
+            if (e->sparse && !e->shard && it < cfg.max_iters) {
+                // next iteration's R = A^T W, speculatively on the side stream next to
+                // this evaluation's gram(W) (both read only W); unused if the loop stops
+                PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+                PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+                e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next);
+                PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
+                e->r_valid = true;
+            }
             const ErrorReport rep = evaluate_error(e);
             ph.error_eval = since(te);
             add_times(totals, ph);
@@ -603,6 +629,7 @@ plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
         if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED) throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
         e->math = math == PLNMF_MATH_EXACT ? Math::exact : Math::fused;
         e->s_valid = false;
+    e->r_valid = false;
     });
 }
 
@@ -722,6 +749,7 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which, con
             PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         }
         if (which == PLNMF_PRODUCT_S) e->s_valid = false;
+    e->r_valid = false;
     });
 }
 
@@ -820,6 +848,7 @@ plnmf_status plnmf_gpu_shard_publish(plnmf_gpu_engine* e) {
                                          cudaMemcpyDeviceToDevice, e->s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         e->s_valid = false;
+    e->r_valid = false;
     });
 }
 
@@ -880,6 +909,7 @@ plnmf_status plnmf_gpu_w_end(plnmf_gpu_engine* e) {
         check_engine(e);
         std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
         e->s_valid = false;
+    e->r_valid = false;
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
     });
 }
@@ -952,6 +982,7 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
         PLNMF_CUDA_CHECK(cudaEventSynchronize(b));
         if (avg_ms) *avg_ms = elapsed_s(a, b) * 1e3 / reps;
         e->s_valid = false;
+    e->r_valid = false;
     });
 }
 

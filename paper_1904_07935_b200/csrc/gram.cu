@@ -21,8 +21,13 @@
 namespace plnmf {
 namespace {
 
+template <class M>
+constexpr bool kExactG = false;
+template <>
+constexpr bool kExactG<MathExact> = true;
+
 constexpr int kGramTile = 32;
-constexpr int kGramRows = 64;  // rows staged per shared-memory chunk (even)
+constexpr int kGramChunk = 32;  // rows of one lane parity staged per shared-memory chunk
 constexpr int kGramBlock = 2048;  // proj/src/linalg.cpp:188 kRowBlock
 constexpr int kGramThreads = 64;  // 8 x 8 threads, 4 x 4 entries each
 
@@ -47,8 +52,11 @@ __global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, 
                                                                   const double* __restrict__ m,
                                                                   double* __restrict__ part,
                                                                   int ntile) {
-    __shared__ double As[kGramRows][kGramTile];
-    __shared__ double Bs[kGramRows][kGramTile];
+    // double-buffered chunks of kGramChunk rows of this lane's parity; cp.async
+    // (16-byte pieces) when k is even, so the next chunk's loads overlap this
+    // chunk's products instead of stalling on the staging loads
+    __shared__ __align__(16) double As[2][kGramChunk][kGramTile];
+    __shared__ __align__(16) double Bs[2][kGramChunk][kGramTile];
     int ta, tb;
     decode_upper(blockIdx.x, ntile, ta, tb);
     const int64_t blk = blockIdx.y >> 1;
@@ -66,22 +74,80 @@ __global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, 
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
 
-    for (int64_t i0 = 0; i0 < cnt; i0 += kGramRows) {
-        const int nr = (int)((cnt - i0) < kGramRows ? (cnt - i0) : kGramRows);
-        for (int idx = threadIdx.x; idx < kGramRows * kGramTile; idx += kGramThreads) {
-            const int rr = idx / kGramTile, cc = idx % kGramTile;
-            const bool rok = rr < nr;
-            const int64_t row = v0 + parity + 2 * (i0 + rr);
-            As[rr][cc] = (rok && a0 + cc < k) ? m[row * k + a0 + cc] : 0.0;
-            Bs[rr][cc] = (rok && b0 + cc < k) ? m[row * k + b0 + cc] : 0.0;
+    const bool vec = (k & 1) == 0;
+    auto stage = [&](int64_t i0, int buf) {
+        const int nr = (int)((cnt - i0) < kGramChunk ? (cnt - i0) : kGramChunk);
+        if (vec) {
+            // 16 pieces of 16 B per row and slice; columns >= k are never read back
+            for (int idx = threadIdx.x; idx < kGramChunk * 32; idx += kGramThreads) {
+                const int sl = idx >> 4 & 1, rr = idx >> 5, u = idx & 15;
+                const int col = (sl ? b0 : a0) + 2 * u;
+                if (rr < nr && col < k) {
+                    const int64_t row = v0 + parity + 2 * (i0 + rr);
+                    double* dst = sl ? &Bs[buf][rr][2 * u] : &As[buf][rr][2 * u];
+                    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(m + row * k + col)
+                                 : "memory");
+                }
+            }
+        } else {
+            for (int idx = threadIdx.x; idx < kGramChunk * kGramTile; idx += kGramThreads) {
+                const int rr = idx / kGramTile, cc = idx % kGramTile;
+                const bool rok = rr < nr;
+                const int64_t row = v0 + parity + 2 * (i0 + rr);
+                As[buf][rr][cc] = (rok && a0 + cc < k) ? m[row * k + a0 + cc] : 0.0;
+                Bs[buf][rr][cc] = (rok && b0 + cc < k) ? m[row * k + b0 + cc] : 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (cnt > 0) stage(0, 0);
+    int cur = 0;
+    for (int64_t i0 = 0; i0 < cnt; i0 += kGramChunk, cur ^= 1) {
+        const int nr = (int)((cnt - i0) < kGramChunk ? (cnt - i0) : kGramChunk);
+        if (i0 + kGramChunk < cnt) {
+            stage(i0 + kGramChunk, cur ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        for (int rr = 0; rr < nr; ++rr) {
+        const double(*Ac)[kGramTile] = As[cur];
+        const double(*Bc)[kGramTile] = Bs[cur];
+        int rr = 0;
+        if (kExactG<M>) {
+            // two rows per step, all 32 products first: every add's multiply is
+            // >= 16 instructions old, and row rr+1's adds follow row rr's per
+            // entry, so each entry's sum keeps the reference's row order
+            for (; rr + 1 < nr; rr += 2) {
+                double av[2][4], bv[2][4], pr[2][4][4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) av[h][i] = Ac[rr + h][ty + 8 * i];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bv[h][j] = Bc[rr + h][tx + 8 * j];
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
+            }
+        }
+        for (; rr < nr; ++rr) {
             double av[4], bv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[rr][ty + 8 * i];
+            for (int i = 0; i < 4; ++i) av[i] = Ac[rr][ty + 8 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[rr][tx + 8 * j];
+            for (int j = 0; j < 4; ++j) bv[j] = Bc[rr][tx + 8 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
