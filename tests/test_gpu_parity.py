@@ -68,6 +68,28 @@ def test_gram_and_spmm_20news_shape_bitwise(gpu):
     assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, f.w))
 
 
+@pytest.mark.parametrize("tile", [16, 22])
+def test_tiled_updates_20news_scale(gpu, tile):
+    """The bench shape (C2, K=240): 77 H rows / 178 W rows per SM, so the
+    staged look-ahead GEMM (lookahead_gemm_private) and the latency-ordered W
+    chain run exactly as in bench.py.  H bitwise; W (norm reduction order
+    only) to 1e-12 from the oracle's own H-updated state."""
+    k = 240
+    m, eng, f = make(**NEWS20, k=k)
+    eng.precompute_h_products()
+    r, s = eng.get_product("r"), eng.get_product("s")
+    cfg = P.SolverConfig(rank=k, tile_size=tile)
+    eng.update_h(cfg, A.tiled)
+    ht1, _ = R.update_tiled(f.ht, s, r, tile, is_w=False)
+    assert bits_equal(eng.get_factors().ht, ht1)
+    eng.precompute_w_products()
+    p, q = eng.get_product("p"), eng.get_product("q")
+    eng.update_w(cfg, A.tiled)
+    w1, norms = R.update_tiled(f.w, q, p, tile, is_w=True)
+    assert rel_max(w1, eng.get_factors().w) <= 1e-12
+    assert elem_rel(norms, eng.get_product("column_norms")) <= 1e-12
+
+
 def _well_conditioned_state(m, k, iters=3, tile=0):
     """Oracle fast-hals trajectory from the seed, to move past the collapse
     of iteration 1 (Finding 1)."""
