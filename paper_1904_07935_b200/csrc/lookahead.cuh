@@ -429,10 +429,12 @@ __device__ __forceinline__ void lookahead_gemm_bulk(const GemmArgs& g, BulkPipe&
 
 namespace plnmf {
 
-// Private-staging variant: each thread stages ITS OWN row's chunk (8-byte
-// aligned rows: cp.async 16 B when k is even) and consumes it, so the ring
-// needs only per-thread cp.async.wait_group — no group barrier.  One row x CG
-// columns per item, items <= count (CG = 16 covers the tile).
+// Private-staging variant: each thread stages its item's row chunk into ITS
+// OWN ring (buffer index = thread; 8-byte aligned rows: cp.async 16 B when k
+// is even) and consumes it, so the ring needs only per-thread
+// cp.async.wait_group — no group barrier, and no buffer is shared between
+// threads (two items of one row live in different threads' rings).  One row x
+// CG columns per item; a thread walks items self, self + count, ... .
 template <class M, int CG, int KC, int ST, int TQC = 0>
 __device__ __forceinline__ void lookahead_gemm_private(const GemmArgs& g) {
     constexpr int KCP = KC + 2;
@@ -442,17 +444,15 @@ __device__ __forceinline__ void lookahead_gemm_private(const GemmArgs& g) {
     const int nitems = g.nrows * ncg;
     const int nch1 = (k - g.en + KC - 1) / KC, nch = nch1 + (g.bprev + KC - 1) / KC;
     const unsigned qb = smem_u32(g.q);
-    const int item = g.self;
-    if (item >= nitems) return;
+    const bool vec = (k & 1) == 0;
+    double* myrow = g.xbuf + g.self * KCP;
+    for (int item = g.self; item < nitems; item += g.count) {
     const int cgi = item / g.nrows, r = item - cgi * g.nrows;
     const int c0 = cgi * CG, cn = min(CG, wn - c0);
-    const bool vec = (k & 1) == 0;
-    // rows of the same row are staged once: only the cgi == 0 item stages it
     auto chunk = [&](int ch, const double*& src, int& kk0, int& n) {
         if (ch < nch1) { src = g.old_m; kk0 = g.en + ch * KC; n = min(KC, k - kk0); }
         else { src = g.out; kk0 = (ch - nch1) * KC; n = min(KC, g.bprev - kk0); }
     };
-    double* myrow = g.xbuf + r * KCP;
     auto stage = [&](int ch) {
         if (ch < nch) {
             const double* src; int kk0, n;
@@ -516,6 +516,7 @@ __device__ __forceinline__ void lookahead_gemm_private(const GemmArgs& g) {
 #pragma unroll
     for (int u = 0; u < CG; ++u)
         if (u < cn) g.dst[r * g.ldt + c0 + u] = a[u];
+    }
 }
 
 }  // namespace plnmf

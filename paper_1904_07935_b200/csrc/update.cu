@@ -60,12 +60,23 @@ int sm_count(int device) {
     return n;
 }
 
+// look-ahead threads of a CTA with `rows` rows (the kernel's warp split)
+int pl_nupd(int64_t rows, bool normalize) {
+    const int row_warps = (int)std::min<int64_t>(8, std::max<int64_t>(1, (rows + 31) / 32));
+    return kLThreads - 32 * (row_warps + (normalize ? 1 : 0));
+}
+// rings of the staged look-ahead GEMM: one per thread that owns items
+int64_t pl_kbuf(int64_t rows, int64_t k, int64_t tile, bool normalize) {
+    const int64_t items = rows * ((std::min<int64_t>(tile, k) + 15) / 16);
+    return std::min<int64_t>(items, pl_nupd(rows, normalize));
+}
 size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem, int kc, int kst = 2,
                bool normalize = false) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
     const int64_t prods = (normalize && tile <= 32) ? rows * tile : 0;  // W chain products (exact path)
+    const int64_t rings = kc > 0 ? kst * pl_kbuf(rows, k, tile, normalize) * (kc + 2) : 0;
     return sizeof(double) * (size_t)((stage_ops ? 4 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
-                                     tile * tile + 48 + 1 + (kc > 0 ? kst * rows * (kc + 2) : 0) + prods);
+                                     tile * tile + 48 + 1 + rings + prods);
 }
 
 // qpanel[tau][kk][j] = coeff(kk, b_tau + j) for j < width(tau), 0 up to TQ.
@@ -205,15 +216,15 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
     plan.kc = 0;
     plan.kst = 0;
     {
-        // the staged GEMM runs one item (row x 16 columns) per look-ahead thread
-        const int row_warps = (int)std::min<int64_t>(8, std::max<int64_t>(1, (rpc + 31) / 32));
-        const int nupd = kLThreads - 32 * (row_warps + (normalize ? 1 : 0));
+        // the staged GEMM runs items (row x 16 columns) round-robin over the look-ahead threads
+        const int nupd = pl_nupd(rpc, normalize);
         const int64_t items = rpc * ((std::min<int64_t>(tile, k) + 15) / 16);
-        if (!std::getenv("PLNMF_NO_STAGED_GEMM") && plan.sqn_smem && items <= nupd)
+        if (!std::getenv("PLNMF_NO_STAGED_GEMM") && plan.sqn_smem && items <= 4 * (int64_t)nupd)
             for (int st : {3, 2})
                 if (pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, kPrivKC, st, normalize) <= (size_t)max_smem) {
                     plan.kc = kPrivKC;
                     plan.kst = st;
+                    plan.kbuf = (int)pl_kbuf(rpc, k, tile, normalize);
                     break;
                 }
     }
@@ -236,7 +247,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                              counters);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
                norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : std::getenv("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1, nullptr,
-               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst,
+               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
                std::getenv("PLNMF_DBG") ? std::atoi(std::getenv("PLNMF_DBG")) : 0};
     {
         const int tq = (int)((tile + 7) & ~int64_t(7));

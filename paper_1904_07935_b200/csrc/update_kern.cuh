@@ -58,6 +58,7 @@ struct LookArgs {
     int sqn_smem;          // 1: the next tile's coeff panel is staged in shared memory
     int kc;                // >0: look-ahead operands staged in kc-wide chunks (lookahead_gemm_private)
     int kst;               // ring depth of those chunks
+    int kbuf;              // rings (one per look-ahead thread that owns items)
     int dbg;               // timing experiments only (PLNMF_DBG bitmask); 0 in production
 };
 
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // look-ahead GEMM operand chunks: p.kst buffers of R x (p.kc + 2), 16-byte aligned
     double* xbuf0 = smem + ((((red + 48) - smem) + 1) & ~(int64_t)1);
     // W chain (exact): per-row products of the next column's old terms, [j][row]
-    double* prodS = xbuf0 + (p.kc > 0 ? (int64_t)p.kst * R * (p.kc + 2) : 0);
+    double* prodS = xbuf0 + (p.kc > 0 ? (int64_t)p.kst * p.kbuf * (p.kc + 2) : 0);
 
     // Profiled threads (look-ahead warp 0, chain warp 0, the exchange warp)
     // add section durations straight to global (profiling runs only); no
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // streaming its own row's operands through a p.kst-deep cp.async ring.
     auto gemm_next = [&](double* dst, int bn, int en, int bprev, int count, int self) {
         GemmArgs ga{dst, ldt, Qn(bn), TQ, bn, en, bprev, p.use_diag, p.old_m, p.out, r0, nrows, k, xbuf0,
-                    R * (kPrivKC + 2), count, self, 2};
+                    p.kbuf * (kPrivKC + 2), count, self, 2};
         if (TQ == 16) {
             if (p.kst >= 3) lookahead_gemm_private<M, 16, kPrivKC, 3, 16>(ga);
             else lookahead_gemm_private<M, 16, kPrivKC, 2, 16>(ga);
