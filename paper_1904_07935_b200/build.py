@@ -28,6 +28,8 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
     "-Xptxas", "-v", "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}",
 ]
+# developer experiments only (e.g. -DPLNMF_CHAIN_ONLY); never set for a real build
+NVCC_FLAGS += os.environ.get("PLNMF_NVCC_EXTRA", "").split()
 HOST_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
               f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
 

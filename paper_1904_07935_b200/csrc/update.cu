@@ -257,9 +257,9 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     }
     static unsigned long long* trace_buf = nullptr;
     if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
-        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 11 * 1024 * 512));
+        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 3 * 1024 * 512));
         a.trace = trace_buf;
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 11 * 1024 * 512, s));
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 3 * 1024 * 512, s));
     }
     if (w_update) {
         exchange_reset(s, k, plan.grid, partials, counters);
@@ -272,7 +272,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     PLNMF_CUDA_CHECK(cudaGetLastError());
     if (a.trace) {
         const int g = plan.grid;
-        std::vector<unsigned long long> h((size_t)11 * k * g);
+        std::vector<unsigned long long> h((size_t)3 * k * g);
         PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
                                          cudaMemcpyDeviceToHost, s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -288,26 +288,6 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
             }
             poll += cp;
             pmax = std::max(pmax, cp / k);
-        }
-        {
-            // chain stamps: [0] row warp released after the exchange, [1] next column's value ready,
-            // [2] its warp partial stored, [3] exchange warp past the reduction barrier, [4] norm published
-            const unsigned long long* c8 = h.data() + (size_t)3 * k * g;
-            double d01 = 0, d12 = 0, d23 = 0, d34 = 0, d40 = 0;
-            int n = 0;
-            for (int64_t t = 0; t + 1 < k; ++t)
-                for (int c = 0; c < g; ++c) {
-                    const unsigned long long* x = c8 + ((size_t)t * g + c) * 8;
-                    const unsigned long long* y = c8 + ((size_t)(t + 1) * g + c) * 8;
-                    if (!x[0] || !x[1] || !y[2] || !y[3] || !y[4]) continue;
-                    d01 += double(x[1] - x[0]); d12 += double(y[2] - x[1]); d23 += double(y[3] - y[2]);
-                    d34 += double(y[4] - y[3]); d40 += double(y[0] - y[4]);
-                    ++n;
-                }
-            if (n)
-                std::fprintf(stderr, "[plnmf] chain stamps (SM cycles): div+next value %.0f, warp reduce %.0f, "
-                             "barrier->exchange warp %.0f, exchange(+partial sum) %.0f, norm->row release %.0f\n",
-                             d01 / n, d12 / n, d23 / n, d34 / n, d40 / n);
         }
         std::fprintf(stderr, "[plnmf] exchange trace (SM cycles/column, mean over CTAs): arrival->complete %.0f "
                      "(max CTA %.0f), complete->partials read %.0f, read->next arrival %.0f\n",

@@ -338,13 +338,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         const double ss = (p.dbg & 8) ? val : warp_sum_lane0(dmul(val, val));
                         if (lane_id() == 0) red[ctid >> 5] = ss;
                     }
-                    unsigned long long* sp8 = p.trace ? p.trace + (size_t)3 * k * gridDim.x +
-                                                            ((size_t)(b + tt) * gridDim.x + blockIdx.x) * 8
-                                                      : nullptr;
-                    if (sp8 && ctid == 0) sp8[2] = clock64();
                     mark(kProfDot);
                     named_sync(1, nchain);
-                    if (sp8 && ctid == nrowt) sp8[3] = clock64();
                     double pre = 0.0, c1 = 0.0, u1 = 0.0;
                     if (is_xwarp) {
                         double blk = 0.0;
@@ -354,12 +349,13 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         }
                         blk = __shfl_sync(0xffffffffu, blk, 0);
                         mark(kProfChain);
-                        const double norm = grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
+                        const double norm = (p.dbg & 32) ? __dsqrt_rn(blk)
+                                                         : grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters,
+                                                                         p.trace);
                         if (lane_id() == 0) {
                             red[40] = norm;
                             if (blockIdx.x == 0) p.norms[b + tt] = norm;
                         }
-                        if (sp8 && lane_id() == 0) sp8[4] = clock64() + (unsigned long long)(norm * 0.0);
                         mark(kProfGrid);
                     } else if (own && !more && has_next) {
                         add_carry = addr[w];  // next tile's first column
@@ -376,11 +372,6 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         mark(kProfUpd);
                     }
                     named_sync(1, nchain);
-                    unsigned long long* st8 = p.trace ? p.trace + (size_t)3 * k * gridDim.x +
-                                                            ((size_t)(b + tt) * gridDim.x + blockIdx.x) * 8
-                                                      : nullptr;
-                    const bool stamp = st8 && ctid == 0;
-                    if (stamp) st8[0] = clock64();
                     const double nv = (p.dbg & 4) ? clamp_floor(p.eps, dmul(val, red[40]))
                                                   : clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
                     if (own) {
@@ -394,7 +385,6 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                             val = clamp_floor(p.eps, dsub(u1, s2));
                         }
                     }
-                    if (stamp) st8[1] = clock64() + (unsigned long long)(val * 0.0);
                     mark(kProfDiv);
                 }
             }
@@ -544,11 +534,14 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             stage_tile(cur ^ 1, bn, en, utid, nupd);
             cp_async_wait<0>();
             named_sync(2, nupd);
+#ifndef PLNMF_CHAIN_ONLY  // timing experiment: the chain with the look-ahead compiled out
             if (p.overlap != 2) build_next(acc[cur ^ 1], bn, en, b, 0, nupd, utid);  // 2: timing probe only
+#endif
             mark(kProfUpd);
         }
         __syncthreads();
         mark(kProfWait);
+#ifndef PLNMF_CHAIN_ONLY
         if (has_next && !p.overlap) {
             load_sqn(bn, en, tid, kLThreads);
             stage_tile(cur ^ 1, bn, en, tid, kLThreads);
@@ -558,10 +551,12 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             __syncthreads();
             mark(kProfUpd);
         }
+#endif
         if (has_next) {
             // ---- boundary: this tile's phase-3 term into the next tile, coeff block of the next tile
             double* An = acc[cur ^ 1];
             const int wn = en - bn, nq = (wn + kLQuad - 1) / kLQuad;
+#ifndef PLNMF_CHAIN_ONLY
             for (int item = tid; item < nrows * nq; item += kLThreads) {
                 const int r = item / nq, cq = (item % nq) * kLQuad;
                 const int wq = min(kLQuad, wn - cq);
@@ -574,6 +569,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 for (int u = 0; u < kLQuad; ++u)
                     if (u < wq) An[r * ldt + cq + u] = a[u];
             }
+#endif
             load_sqc(bn, en, tid, kLThreads);
             __syncthreads();
             mark(kProfBoundary);

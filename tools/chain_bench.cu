@@ -5,6 +5,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1904_07935_b200/csrc \
 //        -o tools/chain_bench.bin tools/chain_bench.cu
 #include <cstdio>
+#include <cstdlib>
 
 #include "exchange.cuh"
 #include "lookahead.cuh"
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(512, 1) chain(int ncol, double* partials, unsi
     if (val == 12345.0) out[0] = val;
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int ncol = 240, g = sms;
@@ -89,12 +90,14 @@ int main() {
                            "+ prefix work", "+ prefix + tile barriers"};
     void* fns[] = {(void*)chain<0, 0, 0>, (void*)chain<0, 1, 0>, (void*)chain<1, 1, 0>, (void*)chain<1, 1, 1>,
                    (void*)chain<1, 1, 1, 1>, (void*)chain<1, 1, 1, 1, 1>};
+    const int dyn = argc > 1 ? atoi(argv[1]) : 0;  // dynamic smem to shrink L1 like the engine kernel
     for (int v = 0; v < 6; ++v) {
+        if (dyn) cudaFuncSetAttribute(fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         for (int rep = 0; rep < 2; ++rep) {
             exchange_reset(0, ncol, g, partials, counters);
             int nc = ncol;
             void* args[] = {&nc, &partials, &counters, &out, &cyc, &add};
-            cudaLaunchCooperativeKernel(fns[v], g, 512, args, 0, 0);
+            cudaLaunchCooperativeKernel(fns[v], g, 512, args, dyn, 0);
             cudaDeviceSynchronize();
         }
         long long h[256];
