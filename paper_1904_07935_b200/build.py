@@ -56,11 +56,15 @@ def _compile(src: Path) -> tuple[Path, str]:
     else:
         cmd = [_cxx(), *HOST_FLAGS, "-c", str(src), "-o", str(obj)]
     deps = [src, *CSRC.glob("*.cuh"), *CSRC.glob("*.hpp"), ROOT / "include" / "plnmf_gpu.h"]
-    if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
+    # the compile command is part of the object's identity (e.g. PLNMF_NVCC_EXTRA experiments)
+    stamp = obj.with_suffix(obj.suffix + ".cmd")
+    same_cmd = stamp.exists() and stamp.read_text() == " ".join(cmd)
+    if same_cmd and obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return obj, ""
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    stamp.write_text(" ".join(cmd))
     return obj, res.stderr
 
 
