@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "lookahead.cuh"
+#include "gemm_variants.cuh"
 
 using namespace plnmf;
 
