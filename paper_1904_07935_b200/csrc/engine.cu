@@ -968,6 +968,10 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
                 case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch); break;
                 case 5: e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch); break;
                 case 6: precompute_w(e); break;  // Q = gram(Ht) || P = A Ht on two streams
+                case 7:  // H-side phase A (init + phase 1 of every tile) into the staging buffer
+                    e->launches += kern::stream_phase_a(e->s, e->math, e->d, e->k, cfg->tile_size, false, e->ht, e->sm,
+                                                        e->staging);
+                    break;
                 case 3:  // successive W updates against the same P, Q (mutates W)
                     update_w(e, *cfg, cfg->tile_size > 0 ? PLNMF_ALGORITHM_TILED : PLNMF_ALGORITHM_REFERENCE);
                     break;
