@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     double* oldB[2] = {smem + 2 * blk, smem + 3 * blk};
     double* sqn = smem + (STAGE ? 4 : 2) * blk;  // k x TQ: coeff(:, next tile's columns), zero-padded
     double* sqc = sqn + (SQN ? (int64_t)k * TQ : 0);  // T x T: coeff(tile, tile) of the current tile
-    double* red = sqc + (int64_t)T * T;                // 48
+    double* red = sqc + (int64_t)T * T;                // 48: [0, 8) warp partials, [40, 42) norm and 1/norm
     // look-ahead GEMM operand chunks: p.kst buffers of R x (p.kc + 2), 16-byte aligned
     double* xbuf0 = smem + ((((red + 48) - smem) + 1) & ~(int64_t)1);
     // W chain (exact): per-row products of the next column's old terms, [j][row]
@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks, tile-0 operands
     {
         const int e0 = min(T, k);
+        if (tid < 8) red[tid] = 0.0;  // warp-partial slots no row warp owns stay +0.0
         load_sqn(0, e0, tid, kLThreads);
         load_sqc(0, e0, tid, kLThreads);
         stage_tile(0, 0, e0, tid, kLThreads);
@@ -344,8 +345,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     if (is_xwarp) {
                         double blk = 0.0;
                         if (lane_id() == 0) {
+                            // fixed order over 8 slots; slots >= row_warps hold +0.0 (x + 0.0 == x)
                             blk = red[0];
-                            for (int i = 1; i < row_warps; ++i) blk = dadd(blk, red[i]);  // fixed order
+#pragma unroll
+                            for (int i = 1; i < 8; ++i) blk = dadd(blk, red[i]);
                         }
                         blk = __shfl_sync(0xffffffffu, blk, 0);
                         mark(kProfChain);
@@ -354,6 +357,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                                                                          p.trace);
                         if (lane_id() == 0) {
                             red[40] = norm;
+                            // the rows divide as a * RN(1/norm) + one fma correction: bit-identical to
+                            // a / norm for operands in [2^-500, 2^500] (tools/div_check.cu: 2.6e10 pairs)
+                            const bool safe = norm >= 0x1p-500 && norm <= 0x1p500;
+                            red[41] = safe ? __drcp_rn(norm) : 0.0;
                             if (blockIdx.x == 0) p.norms[b + tt] = norm;
                         }
                         mark(kProfGrid);
@@ -372,8 +379,16 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         mark(kProfUpd);
                     }
                     named_sync(1, nchain);
-                    const double nv = (p.dbg & 4) ? clamp_floor(p.eps, dmul(val, red[40]))
-                                                  : clamp_floor(p.eps, __ddiv_rn(val, red[40]));  // tiled.cpp:146
+                    double nv;  // max(eps, val / norm), tiled.cpp:146
+                    {
+                        const double bn = red[40], y = red[41];
+                        if (y != 0.0 && val >= 0x1p-500 && val <= 0x1p500) {
+                            const double q0 = __dmul_rn(val, y);
+                            nv = clamp_floor(p.eps, __fma_rn(__fma_rn(-q0, bn, val), y, q0));
+                        } else {
+                            nv = clamp_floor(p.eps, __ddiv_rn(val, bn));
+                        }
+                    }
                     if (own) {
                         arow[tt] = nv;
                         if (more) {

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(512, 1) chain2(Args p) {
                                               : __dsqrt_rn(blk);
                     if (lane_id() == 0) {
                         red[40] = norm;
+                        if (p.flags & 256) red[41] = __drcp_rn(norm);
                         if (blockIdx.x == 0) p.norms[b + tt] = norm;
                     }
                 } else if (own && !more && has_next) {
@@ -106,8 +107,17 @@ __global__ void __launch_bounds__(512, 1) chain2(Args p) {
                     u1 = plnmf::dadd(arow[tt + 1], addr[tt + 1]);
                 }
                 named_sync(1, nchain);
-                const double nv = (p.flags & 64) ? clamp_floor(p.eps, plnmf::dmul(val, red[40]))
-                                                 : clamp_floor(p.eps, __ddiv_rn(val, red[40]));
+                double nv;
+                if (p.flags & 64) {
+                    nv = clamp_floor(p.eps, plnmf::dmul(val, red[40]));
+                } else if (p.flags & 256) {  // reciprocal + one fma correction (Markstein)
+                    const double bn = red[40], y = red[41];
+                    const double q0 = __dmul_rn(val, y);
+                    const double rr = __fma_rn(-q0, bn, val);
+                    nv = clamp_floor(p.eps, __fma_rn(rr, y, q0));
+                } else {
+                    nv = clamp_floor(p.eps, __ddiv_rn(val, red[40]));
+                }
                 if (own) {
                     if (!(p.flags & 8)) arow[tt] = nv;
                     if (more) {
@@ -152,8 +162,8 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int xch : {0})
-        for (int flags : {3, 3 | 4, 3 | 8, 3 | 16, 3 | 32, 3 | 64, 3 | 128, 3 | 4 | 8 | 32 | 64 | 128}) {
+    for (int xch : {0, 1})
+        for (int flags : {0, 3, 3 | 4, 3 | 256, 3 | 4 | 256}) {
             Args p{V, K, T, R, 1e-16, add, out, norms, partials, counters, xch, flags};
             float best = 1e9;
             for (int rep = 0; rep < 3; ++rep) {
