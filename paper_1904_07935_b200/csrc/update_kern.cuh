@@ -253,11 +253,14 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         for (int idx = self; idx < k * TQ / 2; idx += count) cp_async16(sqn + 2 * idx, src + 2 * idx);
         cp_async_commit();
     };
+    // the tile's T x T coefficient block: a sub-block of the staged panel
+    // sqn (coeff(kk, b + j) at sqn[kk * TQ + j]) when that is in shared memory
     auto load_sqc = [&](int b, int e, int self, int count) {
         const int w = e - b;
+        const bool from_panel = SQN && b > 0;  // the panel of tile b is staged during the previous tile
         for (int idx = self; idx < w * w; idx += count) {
             const int i = idx / w, j = idx % w;
-            sqc[i * T + j] = p.coeff[(int64_t)(b + i) * k + b + j];
+            sqc[i * T + j] = from_panel ? sqn[(b + i) * TQ + j] : p.coeff[(int64_t)(b + i) * k + b + j];
         }
     };
 
@@ -570,8 +573,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         if (has_next) {
             // ---- boundary: this tile's phase-3 term into the next tile, coeff block of the next tile
             double* An = acc[cur ^ 1];
-            const int wn = en - bn, nq = (wn + kLQuad - 1) / kLQuad;
+            const int wn = en - bn;
 #ifndef PLNMF_CHAIN_ONLY
+            const int nq = (wn + kLQuad - 1) / kLQuad;
             for (int item = tid; item < nrows * nq; item += kLThreads) {
                 const int r = item / nq, cq = (item % nq) * kLQuad;
                 const int wq = min(kLQuad, wn - cq);
