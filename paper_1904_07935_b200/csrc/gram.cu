@@ -15,6 +15,8 @@
 // proj/src/hals.cpp:29,43 (accumulate_nn / accumulate_tn, linalg.cpp:45-79)
 // with register-tiled SIMT GEMMs in the same per-element order
 // (P: ascending inner index; R: two lanes over all V rows).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -47,8 +49,10 @@ __device__ __forceinline__ void decode_upper(int p, int ntile, int& ta, int& tb)
 // sequential sums in the reference, so they run in separate CTAs (twice the
 // parallelism, half the registers); the combine kernel adds them as
 // (lane0 + 0.0) + lane1 exactly like the compiled reduction.
-template <class M>
-__global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, int k,
+// TJ: entries per thread along b (4: 64 threads per CTA; 2: 128 threads, for short
+// matrices whose (tile, block, lane) count leaves SMs under-occupied)
+template <class M, int TJ = 4, int TI = 4>
+__global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(int64_t n, int k,
                                                                   const double* __restrict__ m,
                                                                   double* __restrict__ part,
                                                                   int ntile) {
@@ -65,21 +69,22 @@ __global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, 
     const int64_t v1 = (v0 + kGramBlock < n) ? v0 + kGramBlock : n;
     // rows of this parity in [v0, v1): v0 + parity + 2i, i < cnt
     const int64_t cnt = (v1 - v0 - parity + 1) / 2;
-    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+    constexpr int NX = 32 / TJ, NY = 32 / TI, NT = NY * NX;  // threads along b / a, per CTA
+    const int tx = threadIdx.x % NX, ty = threadIdx.x / NX;
     const int a0 = ta * kGramTile, b0 = tb * kGramTile;
 
-    double acc[4][4];
+    double acc[TI][TJ];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < TJ; ++j) acc[i][j] = 0.0;
 
     const bool vec = (k & 1) == 0;
     auto stage = [&](int64_t i0, int buf) {
         const int nr = (int)((cnt - i0) < kGramChunk ? (cnt - i0) : kGramChunk);
         if (vec) {
             // 16 pieces of 16 B per row and slice; columns >= k are never read back
-            for (int idx = threadIdx.x; idx < kGramChunk * 32; idx += kGramThreads) {
+            for (int idx = threadIdx.x; idx < kGramChunk * 32; idx += NT) {
                 const int sl = idx >> 4 & 1, rr = idx >> 5, u = idx & 15;
                 const int col = (sl ? b0 : a0) + 2 * u;
                 if (rr < nr && col < k) {
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, 
                 }
             }
         } else {
-            for (int idx = threadIdx.x; idx < kGramChunk * kGramTile; idx += kGramThreads) {
+            for (int idx = threadIdx.x; idx < kGramChunk * kGramTile; idx += NT) {
                 const int rr = idx / kGramTile, cc = idx % kGramTile;
                 const bool rok = rr < nr;
                 const int64_t row = v0 + parity + 2 * (i0 + rr);
@@ -120,47 +125,47 @@ __global__ void __launch_bounds__(kGramThreads, 8) gram_block_kernel(int64_t n, 
             // >= 16 instructions old, and row rr+1's adds follow row rr's per
             // entry, so each entry's sum keeps the reference's row order
             for (; rr + 1 < nr; rr += 2) {
-                double av[2][4], bv[2][4], pr[2][4][4];
+                double av[2][TI], bv[2][TJ], pr[2][TI][TJ];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) av[h][i] = Ac[rr + h][ty + 8 * i];
+                    for (int i = 0; i < TI; ++i) av[h][i] = Ac[rr + h][ty + NY * i];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) bv[h][j] = Bc[rr + h][tx + 8 * j];
+                    for (int j = 0; j < TJ; ++j) bv[h][j] = Bc[rr + h][tx + NX * j];
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
+                        for (int j = 0; j < TJ; ++j) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
+                        for (int j = 0; j < TJ; ++j) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
             }
         }
         for (; rr < nr; ++rr) {
-            double av[4], bv[4];
+            double av[TI], bv[TJ];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = Ac[rr][ty + 8 * i];
+            for (int i = 0; i < TI; ++i) av[i] = Ac[rr][ty + NY * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bc[rr][tx + 8 * j];
+            for (int j = 0; j < TJ; ++j) bv[j] = Bc[rr][tx + NX * j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < TI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
+                for (int j = 0; j < TJ; ++j) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
         }
         __syncthreads();
     }
     double* pb = part + (int64_t)blockIdx.y * k * k;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int a = a0 + ty + 8 * i, b = b0 + tx + 8 * j;
+        for (int j = 0; j < TJ; ++j) {
+            const int a = a0 + ty + NY * i, b = b0 + tx + NX * j;
             if (a < k && b < k) pb[(int64_t)a * k + b] = acc[i][j];
         }
 }
@@ -315,10 +320,21 @@ int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double
     }
     const int ntile = (int)((k + kGramTile - 1) / kGramTile);
     const dim3 grid((unsigned)(ntile * (ntile + 1) / 2), (unsigned)(2 * nblk));
-    if (m == Math::exact)
-        gram_block_kernel<MathExact><<<grid, kGramThreads, 0, s>>>(n, (int)k, mat, scratch, ntile);
-    else
-        gram_block_kernel<MathFused><<<grid, kGramThreads, 0, s>>>(n, (int)k, mat, scratch, ntile);
+    // fewer than ~4 CTAs per SM of 4x4 threads: use 4x2 threads (twice the warps)
+    int dev = 0, sms = 148;
+    PLNMF_CUDA_CHECK(cudaGetDevice(&dev));
+    PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const bool narrow = (int64_t)grid.x * grid.y < 8LL * sms;
+    const int variant = std::getenv("PLNMF_GRAM_TILE") ? std::atoi(std::getenv("PLNMF_GRAM_TILE")) : (narrow ? 42 : 44);
+    if (m == Math::exact) {
+        if (variant == 22) gram_block_kernel<MathExact, 2, 2><<<grid, 256, 0, s>>>(n, (int)k, mat, scratch, ntile);
+        else if (variant == 42) gram_block_kernel<MathExact, 2, 4><<<grid, 128, 0, s>>>(n, (int)k, mat, scratch, ntile);
+        else gram_block_kernel<MathExact, 4, 4><<<grid, 64, 0, s>>>(n, (int)k, mat, scratch, ntile);
+    } else {
+        if (variant == 22) gram_block_kernel<MathFused, 2, 2><<<grid, 256, 0, s>>>(n, (int)k, mat, scratch, ntile);
+        else if (variant == 42) gram_block_kernel<MathFused, 2, 4><<<grid, 128, 0, s>>>(n, (int)k, mat, scratch, ntile);
+        else gram_block_kernel<MathFused, 4, 4><<<grid, 64, 0, s>>>(n, (int)k, mat, scratch, ntile);
+    }
     PLNMF_CUDA_CHECK(cudaGetLastError());
     const int64_t tot = k * k;
     gram_combine_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((int)k, nblk, scratch, g);
