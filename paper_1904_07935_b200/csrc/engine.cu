@@ -198,7 +198,7 @@ void precompute_w(plnmf_gpu_engine* e) {
     e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
     if (e->sparse)
         e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
-                                      e->k, e->p);
+                                      e->k, e->p, e->nnz);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
     PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
@@ -961,7 +961,7 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
         auto once = [&] {
             switch (which) {
                 case 0:
-                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p);
+                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p, e->nnz);
                     else e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
                     break;
                 case 1:

@@ -30,8 +30,9 @@ namespace kern {
 // y := a * x over CSR a (rows x ?), x row-major (? x k), y row-major (rows x k).
 // Per element: acc = 0; acc += val[e] * x[col[e]][j] for e ascending —
 // proj/src/linalg.cpp:139-154.
+// nnz: the matrix's nonzero count (selects the unroll depth; -1 if unknown).
 int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
-             const double* val, const double* x, int64_t k, double* y);
+             const double* val, const double* x, int64_t k, double* y, int64_t nnz = -1);
 
 // g := m^T m (k x k) for row-major m (n x k), in the reference's compiled
 // order (2048-row blocks, even/odd lanes, proj/src/linalg.cpp:168-204).

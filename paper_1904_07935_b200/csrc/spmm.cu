@@ -20,8 +20,8 @@ namespace {
 constexpr int kSpmmThreads = 256;
 constexpr int kUnroll = 4;
 
-template <int NC, class M>
-__global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(
+template <int NC, class M, int UNR = kUnroll, int MINB = 1>
+__global__ void __launch_bounds__(kSpmmThreads, MINB) spmm_csr_kernel(
     int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
     const double* __restrict__ val, const double* __restrict__ x, int64_t ldx,
     double* __restrict__ y, int64_t ldy, int col0, int ncols) {
@@ -48,11 +48,11 @@ __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(
             a = __ldg(val + base + lane);
         }
         int i = 0;
-        for (; i + kUnroll <= cnt; i += kUnroll) {
-            double xv[kUnroll][NC];
-            double av[kUnroll];
+        for (; i + UNR <= cnt; i += UNR) {
+            double xv[UNR][NC];
+            double av[UNR];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < UNR; ++u) {
                 const int cc = __shfl_sync(0xffffffffu, c, i + u);
                 av[u] = __shfl_sync(0xffffffffu, a, i + u);
                 const double* xr = xb + (int64_t)cc * ldx;
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(
                 for (int g = 0; g < NC; ++g) xv[u][g] = ok[g] ? __ldg(xr + kWarp * g) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+            for (int u = 0; u < UNR; ++u)
 #pragma unroll
                 for (int g = 0; g < NC; ++g) acc[g] = M::madd(acc[g], av[u], xv[u][g]);
         }
@@ -81,13 +81,21 @@ __global__ void __launch_bounds__(kSpmmThreads) spmm_csr_kernel(
 
 template <class M>
 void launch_pass(cudaStream_t s, int nc, int64_t rows, const int64_t* rp, const int32_t* ci,
-                 const double* val, const double* x, int64_t k, double* y, int col0, int ncols) {
+                 const double* val, const double* x, int64_t k, double* y, int col0, int ncols, bool short_rows) {
     const dim3 grid((unsigned)((rows + kSpmmThreads / kWarp - 1) / (kSpmmThreads / kWarp)));
 #define PLNMF_SPMM_CASE(N)                                                                   \
     case N:                                                                                  \
         spmm_csr_kernel<N, M><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k,   \
                                                             col0, ncols);                    \
         break;
+    // short rows (few nonzeros to unroll over): a 2-deep unroll at 80 registers
+    // runs 3 CTAs per SM (24 warps) and keeps more gathers in flight than 2 CTAs
+    // of a 4-deep unroll (A*Ht at C2: 126 vs 134 us; A^T*W's longer rows prefer 4)
+    if (nc == 8 && short_rows) {
+        spmm_csr_kernel<8, M, 2, 3><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols);
+        PLNMF_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     switch (nc) {
         PLNMF_SPMM_CASE(1)
         PLNMF_SPMM_CASE(2)
@@ -108,8 +116,9 @@ void launch_pass(cudaStream_t s, int nc, int64_t rows, const int64_t* rp, const 
 namespace kern {
 
 int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
-             const double* val, const double* x, int64_t k, double* y) {
+             const double* val, const double* x, int64_t k, double* y, int64_t nnz) {
     if (rows <= 0 || k <= 0) return 0;
+    const bool short_rows = nnz >= 0 && nnz < 60 * rows;  // mean < 60 nonzeros per row
     // Columns are processed in passes of at most 256 (8 warp-wide groups);
     // passes split K evenly so no pass is nearly empty.
     const int64_t passes = (k + 255) / 256;
@@ -119,9 +128,9 @@ int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int3
         const int ncols = (int)((k - c0) < per ? (k - c0) : per);
         const int nc = (ncols + kWarp - 1) / kWarp;
         if (m == Math::exact)
-            launch_pass<MathExact>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols);
+            launch_pass<MathExact>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows);
         else
-            launch_pass<MathFused>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols);
+            launch_pass<MathFused>(s, nc, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows);
         ++launches;
     }
     return launches;
