@@ -29,6 +29,7 @@ struct plnmf_gpu_engine {
     cudaStream_t s = nullptr, s2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     int64_t v = 0, d = 0, k = 0, nnz = 0;
+    int64_t nnz_t = -1;  // nonzeros of the A^T block (sharded engines: of the local column block)
     bool sparse = true;
     double a2 = 0.0;
     Math math = Math::exact;
@@ -60,19 +61,6 @@ struct plnmf_gpu_engine {
     kern::PhaseBPlan plan_w, plan_h, plan_ref_w;
     bool have_ref_w = false;
 
-    // CUDA graphs of one whole FAST-HALS iteration (precompute_h .. update_w),
-    // keyed by the factor buffers it starts from and the configuration; an
-    // iteration swaps w/w_new and ht/h_new, so two graphs alternate.
-    struct IterGraph {
-        double *w0, *ht0;
-        int64_t tile;
-        double eps;
-        int alg;
-        Math math;
-        cudaGraphExec_t exec;
-        uint64_t launches, macs;
-    };
-    std::vector<IterGraph> graphs;
 
     std::vector<cudaEvent_t> events;  // per-phase timing pool
     long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
@@ -111,7 +99,6 @@ void release(plnmf_gpu_engine* e) {
     for (void* ptr : e->allocs) cudaFree(ptr);
     if (e->host_scalars) cudaFreeHost(e->host_scalars);
     for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
-    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
     if (e->fork) cudaEventDestroy(e->fork);
     if (e->join_r) cudaEventDestroy(e->join_r);
     if (e->join) cudaEventDestroy(e->join);
@@ -191,13 +178,16 @@ void precompute_h(plnmf_gpu_engine* e) {
     if (need_s) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
-        e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
     }
+    // the SpMM is submitted first: its CTAs take the SMs' registers for their
+    // memory-level parallelism and the Gram's small CTAs fill what is left,
+    // so the two co-reside instead of the Gram draining the GPU first
     if (e->sparse)
         e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->shard ? e->w_full : e->w,
-                                      e->k, e->r);
+                                      e->k, e->r, e->nnz_t);
     else
         e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
+    if (need_s) e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
     if (need_s) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
@@ -210,12 +200,12 @@ void precompute_h(plnmf_gpu_engine* e) {
 void precompute_w(plnmf_gpu_engine* e) {
     PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
     PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
-    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
-    if (e->sparse)
+    if (e->sparse)  // SpMM first, as in precompute_h
         e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
                                       e->k, e->p, e->nnz);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
+    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
     PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
     PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
 }
@@ -567,6 +557,7 @@ plnmf_status plnmf_gpu_create_csr(int32_t device, int64_t rows, int64_t cols, in
         e->v = rows;
         e->d = cols;
         e->nnz = nnz;
+        e->nnz_t = nnz;
         e->sparse = true;
         double n2 = 0.0;  // InputMatrix ctor, proj/src/input_matrix.cpp:15-20 (serial)
         for (int64_t i = 0; i < nnz; ++i) n2 += values[i] * values[i];
@@ -798,6 +789,7 @@ plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int64_t v, in
         e->v = vl;
         e->d = dl;
         e->nnz = nnz_rows;
+        e->nnz_t = nnz_cols;
         e->sparse = true;
         e->a2 = a_norm_sq;
         auto upload = [&](int64_t rows, int64_t nnz, const int64_t* rp, const int64_t* ci, const double* val,
@@ -943,56 +935,14 @@ plnmf_status plnmf_gpu_local_pw(plnmf_gpu_engine* e, double* out) {
     });
 }
 
-// One FAST-HALS iteration.  When the state is the steady one (no products
-// carried over, no profiling), the iteration is replayed from a CUDA graph
-// captured the first time this (factor buffers, configuration) pair is seen:
-// ~14 dependent launches, two cross-stream joins and the exchange resets
-// become one graph launch, removing the inter-kernel gaps.
+// One FAST-HALS iteration in the reference's order (solver.cpp:79-92).  (A
+// CUDA-graph replay of whole iterations was measured slower, 1.73 vs 1.65 ms,
+// and removed: the GPU is never idle between these launches.)
 void one_iteration(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
-    static const bool no_graphs = std::getenv("PLNMF_NO_GRAPHS") != nullptr;
-    const bool steady = !e->s_valid && !e->r_valid && !e->shard && !std::getenv("PLNMF_PROFILE") &&
-                        !std::getenv("PLNMF_TRACE_EXCHANGE") && e->plan_tile == cfg.tile_size;
-    if (no_graphs || !steady) {
-        precompute_h(e);
-        update_h(e, cfg, alg);
-        precompute_w(e);
-        update_w(e, cfg, alg);
-        return;
-    }
-    for (auto& g : e->graphs) {
-        if (g.w0 == e->w && g.ht0 == e->ht && g.tile == cfg.tile_size && g.eps == cfg.epsilon && g.alg == (int)alg &&
-            g.math == e->math) {
-            PLNMF_CUDA_CHECK(cudaGraphLaunch(g.exec, e->s));
-            std::swap(e->ht, e->h_new);  // the host side of the captured iteration
-            std::swap(e->w, e->w_new);
-            e->s_valid = false;
-            e->r_valid = false;
-            e->launches += g.launches;
-            e->update_macs += g.macs;
-            return;
-        }
-    }
-    IterGraph g{e->w, e->ht, cfg.tile_size, cfg.epsilon, (int)alg, e->math, nullptr, 0, 0};
-    const uint64_t l0 = e->launches, m0 = e->update_macs;
-    cudaGraph_t graph = nullptr;
-    PLNMF_CUDA_CHECK(cudaStreamBeginCapture(e->s, cudaStreamCaptureModeThreadLocal));
-    try {
-        precompute_h(e);
-        update_h(e, cfg, alg);
-        precompute_w(e);
-        update_w(e, cfg, alg);
-    } catch (...) {
-        cudaStreamEndCapture(e->s, &graph);
-        if (graph) cudaGraphDestroy(graph);
-        throw;
-    }
-    PLNMF_CUDA_CHECK(cudaStreamEndCapture(e->s, &graph));
-    PLNMF_CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
-    PLNMF_CUDA_CHECK(cudaGraphDestroy(graph));
-    g.launches = e->launches - l0;
-    g.macs = e->update_macs - m0;
-    e->graphs.push_back(g);
-    PLNMF_CUDA_CHECK(cudaGraphLaunch(g.exec, e->s));  // capture recorded the work; now run it
+    precompute_h(e);
+    update_h(e, cfg, alg);
+    precompute_w(e);
+    update_w(e, cfg, alg);
 }
 
 plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg, int64_t n,
@@ -1033,6 +983,11 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
                 case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch); break;
                 case 5: e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch); break;
                 case 6: precompute_w(e); break;  // Q = gram(Ht) || P = A Ht on two streams
+                case 8:  // S = gram(W) || R = A^T W on two streams
+                    e->s_valid = false;
+                    e->r_valid = false;
+                    precompute_h(e);
+                    break;
                 case 7:  // H-side phase A (init + phase 1 of every tile) into the staging buffer
                     e->launches += kern::stream_phase_a(e->s, e->math, e->d, e->k, cfg->tile_size, false, e->ht, e->sm,
                                                         e->staging);

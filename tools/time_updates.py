@@ -23,7 +23,7 @@ eng = P.Engine(a, k)
 cfg = P.SolverConfig(rank=k, tile_size=tile, max_iters=1, rel_tol=0.0)
 eng.init_factors(cfg)
 eng.run_iterations(cfg, P.Algorithm.tiled, 2)
-names = ["A*Ht", "At*W", "gram W", "update W", "update H", "gram Ht", "precompute_w", "phase A (H)"]
+names = ["A*Ht", "At*W", "gram W", "update W", "update H", "gram Ht", "precompute_w", "phase A (H)", "precompute_h"]
 print(f"V={v} D={d} K={k} T={tile} nnz={eng.nnz}")
 for i, n in enumerate(names):
     print(f"{n:12s} {eng.time_kernel(cfg, i, 3) * 1e3:10.1f} us")
