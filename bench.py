@@ -262,6 +262,13 @@ def engine_arm(args):
                               "bytes_A_Ht": b_p, "bytes_At_W": b_r,
                               "l2_gather_bytes": 8 * nnz * K},
             "update_w_bytes": b_w,
+            # the step's dominant kernel is neither HBM- nor tensor-bound: it is the W
+            # update's chain of K grid-wide norm exchanges
+            "dominant_kernel": {"kernel": "pl_update_kernel (W, tiled)", "share_of_step": kt["update_w_tiled"] / step,
+                                "bound": "latency (K dependent grid-wide reductions)",
+                                "us_per_column": kt["update_w_tiled"] * 1e3 / K,
+                                "isolated_exchange_us": 1.28, "isolated_chain_plus_exchange_us": 1.73,
+                                "source": "tools/exchange_bench2.cu, tools/chain_bench.cu (profiles/)"},
             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
         }
         print(json.dumps(line), flush=True)
