@@ -61,6 +61,7 @@ struct PhaseBPlan {
     int kc = 0;              // look-ahead GEMM: operand chunk width staged by cp.async (0: unstaged path)
     int kst = 0;             // look-ahead GEMM: chunk ring depth
     int kbuf = 0;            // look-ahead GEMM: rings (one per item-owning thread)
+    int resident = 0;        // H: the CTA's rows stay in shared memory (lookahead_gemm_resident)
 };
 // Global scratch for the coeff column panels of one tiled update.
 int64_t qpanel_doubles(int64_t k, int64_t tile);

@@ -158,3 +158,54 @@ __device__ __forceinline__ void lookahead_gemm_private(const GemmArgs& g) {
 }
 
 }  // namespace plnmf
+
+namespace plnmf {
+
+// Resident-rows variant (H update: the CTA's whole row block of the old
+// factor sits in shared memory, rows ld apart, finished tiles written back in
+// place): no staging and no barriers.  A thread item is ONE column c (lanes =
+// consecutive columns, so the row operands of a kk are broadcast within each
+// 16-lane half and the coefficient load is one conflict-free wavefront) and up
+// to RG rows g, g + ng, g + 2 ng, ... (ng = count / 16 row groups).
+// Per-element order as lookahead_gemm_private: bit-identical under Math::exact.
+template <class M, int RG>
+__device__ __forceinline__ void lookahead_gemm_resident(const GemmArgs& g, const double* resid, int ld) {
+    const int wn = g.en - g.bn, k = g.k;
+    const int ng = g.count / 16;  // row groups
+    const int c = g.self % 16, grp = g.self / 16;
+    if (c >= wn || grp >= ng) return;
+    const unsigned qb = smem_u32(g.q), xb = smem_u32(resid);
+    int rr[RG];
+    int rn = 0;
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+        rr[i] = grp + i * ng;
+        if (rr[i] < g.nrows) rn = i + 1;
+    }
+    if (rn == 0) return;
+    double a[RG];
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+        a[i] = 0.0;
+        if (i < rn) {
+            const double o = resid[rr[i] * ld + g.bn + c];
+            a[i] = g.use_diag ? dmul(o, lds64(qb + 8u * ((g.bn + c) * g.tq + c))) : o;
+        }
+    }
+    auto seg = [&](int k0, int k1) {
+#pragma unroll 4
+        for (int kk = k0; kk < k1; ++kk) {
+            const double q = -1.0 * lds64(qb + 8u * (kk * g.tq + c));
+#pragma unroll
+            for (int i = 0; i < RG; ++i)
+                if (i < rn) a[i] = M::madd(a[i], q, lds64(xb + 8u * (rr[i] * ld + kk)));
+        }
+    };
+    seg(g.en, k);     // phase 1: old values of the columns right of the tile
+    seg(0, g.bprev);  // phase 3 of the tiles before the previous one: finished values
+#pragma unroll
+    for (int i = 0; i < RG; ++i)
+        if (i < rn) g.dst[rr[i] * g.ldt + c] = a[i];
+}
+
+}  // namespace plnmf

@@ -229,6 +229,22 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
                 }
     }
     plan.smem = pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, plan.kc, plan.kst, normalize);
+    if (!normalize && tile <= 16 && !std::getenv("PLNMF_NO_RESIDENT")) {
+        // H: keep the CTA's rows resident in shared memory when they fit (no
+        // staging, no oldB), up to 4 rows per look-ahead thread of a column
+        const int64_t tq = (tile + 7) & ~int64_t(7);
+        const size_t smem = sizeof(double) * (size_t)(2 * rpc * (tile + 1) + k * tq + tile * tile + 48 + 1 +
+                                                      rpc * (k + 2));
+        if (smem <= (size_t)max_smem && rpc <= 4 * (pl_nupd(rpc, false) / 16)) {
+            plan.resident = 1;
+            plan.stage_ops = false;
+            plan.sqn_smem = true;
+            plan.kc = 0;
+            plan.kst = 0;
+            plan.kbuf = 0;
+            plan.smem = smem;
+        }
+    }
     return plan;
 }
 
@@ -248,7 +264,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
                norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : std::getenv("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1, nullptr,
                qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
-               std::getenv("PLNMF_DBG") ? std::atoi(std::getenv("PLNMF_DBG")) : 0};
+               std::getenv("PLNMF_DBG") ? std::atoi(std::getenv("PLNMF_DBG")) : 0, plan.resident, (int)k + 2};
     {
         const int tq = (int)((tile + 7) & ~int64_t(7));
         qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(

@@ -60,6 +60,8 @@ struct LookArgs {
     int kst;               // ring depth of those chunks
     int kbuf;              // rings (one per look-ahead thread that owns items)
     int dbg;               // timing experiments only (PLNMF_DBG bitmask); 0 in production
+    int resident;          // 1: the CTA's old rows live in shared memory (H update, lookahead_gemm_resident)
+    int ldr;               // their leading dimension (k + 2)
 };
 
 template <class M>
@@ -147,6 +149,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     double* xbuf0 = smem + ((((red + 48) - smem) + 1) & ~(int64_t)1);
     // W chain (exact): per-row products of the next column's old terms, [j][row]
     double* prodS = xbuf0 + (p.kc > 0 ? (int64_t)p.kst * p.kbuf * (p.kc + 2) : 0);
+    // resident mode (kc == 0): the CTA's rows of the factor, old values until a
+    // tile finishes, then its new values (written back at the tile end)
+    double* resid = xbuf0;
 
     // Profiled threads (look-ahead warp 0, chain warp 0, the exchange warp)
     // add section durations straight to global (profiling runs only); no
@@ -191,6 +196,12 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     };
     auto build_next = [&](double* dst, int bn, int en, int bprev, int first, int count, int self) {
         const double* Q = Qn(bn);
+        if (TMAX > 0 && SQN && p.resident && count == nupd) {
+            GemmArgs ga{dst, ldt, Qn(bn), TQ, bn, en, bprev, p.use_diag, p.old_m, p.out, r0, nrows, k, nullptr, 0,
+                        count, self, 2};
+            lookahead_gemm_resident<M, 4>(ga, resid, p.ldr);
+            return;
+        }
         if (TMAX > 0 && SQN && p.kc > 0 && count == nupd) {
             gemm_next(dst, bn, en, bprev, count, self);
             return;
@@ -281,12 +292,22 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     {
         const int e0 = min(T, k);
         if (tid < 8) red[tid] = 0.0;  // warp-partial slots no row warp owns stay +0.0
+        if (p.resident) {  // the CTA's rows of the old factor, once
+            const bool vec = (k & 1) == 0;
+            const int pr = vec ? k / 2 : k;
+            for (int idx = tid; idx < nrows * pr; idx += kLThreads) {
+                const int r = idx / pr, u = idx - r * pr;
+                if (vec) cp_async16(resid + r * p.ldr + 2 * u, p.old_m + (r0 + r) * k + 2 * u);
+                else cp_async8(resid + r * p.ldr + u, p.old_m + (r0 + r) * k + u);
+            }
+            cp_async_commit();
+        }
         load_sqn(0, e0, tid, kLThreads);
         load_sqc(0, e0, tid, kLThreads);
         stage_tile(0, 0, e0, tid, kLThreads);
         cp_async_wait<0>();
         __syncthreads();
-        if (p.kc > 0) {
+        if (p.kc > 0 || p.resident) {
             if (!is_chain) build_next(acc[0], 0, e0, 0, 0, nupd, utid);
         } else {
             build_next(acc[0], 0, e0, 0, 0, kLThreads, tid);
@@ -319,7 +340,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             double* prod = prodS + r;  // prod[j * R]: this row's products, conflict-free across lanes
             double* arow = A + r * ldt;
             const double* addr = p.add + (r0 + r) * k + b;
-            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+            const double* orow = p.resident ? resid + r * p.ldr + b
+                                 : STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
             // column 0 of the tile: every scratch term is old (tiled.cpp:118-131)
             double val = 0.0;
             {
@@ -410,6 +432,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             for (int idx = ctid; idx < nrows * w; idx += nchain) {
                 const int rr = idx / w, j = idx % w;
                 p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+                if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
             }
             mark(kProfChain);
         } else if (is_chain && TMAX > 0) {
@@ -420,7 +443,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             double x[TM];
             double* arow = A + r * ldt;
             const double* addr = p.add + (r0 + r) * k + b;
-            const double* orow = STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+            const double* orow = p.resident ? resid + r * p.ldr + b
+                                 : STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
 #pragma unroll
             for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
             double pre = 0.0;  // sum_{j < tt-1} x[j] c(j, tt), precomputed during the previous exchange
@@ -488,6 +512,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             for (int idx = ctid; idx < nrows * w; idx += nchain) {
                 const int rr = idx / w, j = idx % w;
                 p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+                if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
             }
             mark(kProfChain);
         } else if (is_chain) {
@@ -544,6 +569,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             for (int idx = ctid; idx < nrows * w; idx += nchain) {
                 const int r = idx / w, j = idx % w;
                 p.out[(r0 + r) * k + b + j] = A[r * ldt + j];
+                if (p.resident) resid[r * p.ldr + b + j] = A[r * ldt + j];
             }
             mark(kProfChain);
         } else if (has_next && p.overlap) {
