@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         if (TMAX > 0 && SQN && p.resident && count == nupd) {
             GemmArgs ga{dst, ldt, Qn(bn), TQ, bn, en, bprev, p.use_diag, p.old_m, p.out, r0, nrows, k, nullptr, 0,
                         count, self, 2};
-            lookahead_gemm_resident<M, 4>(ga, resid, p.ldr);
+            const int rg = (nrows + count / 16 - 1) / (count / 16);  // rows per thread (<= 4 by the planner)
+            if (rg <= 2) lookahead_gemm_resident<M, 2>(ga, resid, p.ldr);
+            else if (rg == 3) lookahead_gemm_resident<M, 3>(ga, resid, p.ldr);
+            else lookahead_gemm_resident<M, 4>(ga, resid, p.ldr);
             return;
         }
         if (TMAX > 0 && SQN && p.kc > 0 && count == nupd) {
