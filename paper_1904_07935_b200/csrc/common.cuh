@@ -40,6 +40,27 @@ __device__ __forceinline__ double warp_sum_lane0(double v) {
     return v;
 }
 
+// a / b, correctly rounded, as an out-of-line call: for rare paths inside
+// latency-critical loops whose code must stay small (the instruction cache)
+static __device__ __noinline__ double div_outlined(double a, double b) { return __ddiv_rn(a, b); }
+
+// Fixed pairwise tree over 8 values (3 dependent adds instead of 7).
+__device__ __forceinline__ double tree8(const double (&v)[8]) {
+    return dadd(dadd(dadd(v[0], v[1]), dadd(v[2], v[3])), dadd(dadd(v[4], v[5]), dadd(v[6], v[7])));
+}
+
+// Deterministic warp sum with the result in every lane: an xor butterfly.
+// IEEE addition is commutative, so lanes l and l^off form the same sum at
+// every level and all lanes end with identical bits (no broadcast shuffle).
+// Shared-memory trees are slower here: the exchange warp shares the MIO pipe
+// with the look-ahead warps' shared-memory traffic (measured: +400 us per W
+// update with a 32-load tree).
+__device__ __forceinline__ double warp_sum_all(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
 // Deterministic block sum (fixed tree); every thread gets the value.
 // scratch must hold >= blockDim.x/32 + 1 doubles.
 __device__ __forceinline__ double block_sum(double v, double* scratch) {

@@ -14,16 +14,18 @@ namespace plnmf {
 // every replica's arrival counter with a relaxed red; it then polls the
 // counter of replica (cta % kReplicas) until all g CTAs have arrived, loads
 // that replica's g partials at once (re-polling any slot still NaN) and sums
-// them in one fixed order — lane l adds partials l, l+32, ... in order, then a
-// fixed shuffle tree — so every CTA computes the bit-identical sum, run to
-// run.  Replication spreads the 148-way read of the same bytes over kReplicas
-// groups of L2 lines (one copy per ~18 CTAs): with a single copy, those reads
-// serialise at the L2 slices and skew the next column's arrivals by ~2.5 us
-// (measured with PLNMF_TRACE_EXCHANGE).
+// them in one fixed order — lane l adds partials l, l+32, ... in a pairwise
+// tree, then an xor butterfly over the lanes (warp_sum_all) — so every CTA
+// computes the bit-identical sum, run to run.  Replication
+// spreads the 148-way read of the same bytes over kReplicas groups of L2
+// lines (one copy per ~18 CTAs): with a single copy, those reads serialise at
+// the L2 slices and skew the next column's arrivals by ~2.5 us (measured with
+// PLNMF_TRACE_EXCHANGE).
 // Layout: partials[(t * kReplicas + rep) * stride + cta], counters[(t * kReplicas + rep) * 64].
 constexpr int kMaxPartialsPerLane = 8;  // g <= 256 CTAs
 constexpr int kReplicas = 8;
 constexpr int kCounterStride = 64;      // 256 B between replica counters
+constexpr int kTraceSlots = 16;         // PLNMF_TRACE_EXCHANGE stamps per (column, CTA)
 
 __host__ __device__ inline int64_t partial_stride(int g) { return ((g + 31) / 32) * 32 + 32; }
 inline int64_t xch_partials(int64_t k, int g) { return k * kReplicas * partial_stride(g); }
@@ -39,12 +41,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // PLNMF_TRACE_EXCHANGE): per column and CTA the SM clock at arrival, at
 // counter completion, and after the partials are read.
 __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
-                                unsigned long long* trace = nullptr) {
+                                                unsigned long long* trace = nullptr) {
+    static_assert(kMaxPartialsPerLane == 8, "tree8 sums the partials of one lane");
     const int lane = lane_id();
     const int64_t stride = partial_stride(g);
     double* base = partials + (int64_t)t * kReplicas * stride;
     unsigned* cbase = counters + (int64_t)t * kReplicas * kCounterStride;
-    unsigned long long* tr = trace ? trace + ((int64_t)t * g + blockIdx.x) * 3 : nullptr;
+    unsigned long long* tr = trace ? trace + ((int64_t)t * g + blockIdx.x) * kTraceSlots : nullptr;
     if (tr && lane == 0) tr[0] = clock64();
     if (lane < kReplicas) {
         st_relaxed_f64(base + lane * stride + blockIdx.x, blk);
@@ -73,12 +76,9 @@ __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double
         for (int i = 0; i < kMaxPartialsPerLane; ++i)
             if (isnan(v[i])) v[i] = ld_relaxed_f64(col + lane + kWarp * i);
     }
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < kMaxPartialsPerLane; ++i) s = dadd(s, v[i]);
-    s = warp_sum_lane0(s);
+    const double s = warp_sum_all(tree8(v));
     if (tr && lane == 0) tr[2] = clock64();
-    return __shfl_sync(0xffffffffu, __dsqrt_rn(s), 0);
+    return __dsqrt_rn(s);
 }
 
 

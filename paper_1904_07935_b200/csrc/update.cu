@@ -273,9 +273,9 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     }
     static unsigned long long* trace_buf = nullptr;
     if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
-        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * 3 * 1024 * 512));
+        if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * kTraceSlots * 1024 * 512));
         a.trace = trace_buf;
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 3 * 1024 * 512, s));
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * kTraceSlots * 1024 * 512, s));
     }
     if (w_update) {
         exchange_reset(s, k, plan.grid, partials, counters);
@@ -288,26 +288,53 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
     PLNMF_CUDA_CHECK(cudaGetLastError());
     if (a.trace) {
         const int g = plan.grid;
-        std::vector<unsigned long long> h((size_t)3 * k * g);
+        std::vector<unsigned long long> h((size_t)kTraceSlots * k * g);
         PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
                                          cudaMemcpyDeviceToHost, s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
-        // SM-clock durations per CTA (clocks are per SM: only same-CTA differences are meaningful)
-        double poll = 0, read = 0, gap = 0, pmax = 0;
-        for (int c = 0; c < g; ++c) {
-            double cp = 0;
-            for (int64_t t = 0; t < k; ++t) {
-                const unsigned long long* x = &h[(size_t)(t * g + c) * 3];
-                cp += double(x[1] - x[0]);
-                read += double(x[2] - x[1]);
-                if (t > 0) gap += double(x[0] - h[(size_t)((t - 1) * g + c) * 3 + 2]);
+        // SM-clock durations per CTA (clocks are per SM: only same-CTA differences are meaningful).
+        // Stamps: 0 arrival, 1 counter complete, 2 partials read (exchange warp); 3 exchange warp
+        // past the norm barrier; 4 chain warp 0 past the norm barrier, 5 its next value done,
+        // 6 its square reduced and parked; 7 exchange warp has the CTA partial.
+        const int S = kTraceSlots;
+        auto span = [&](bool boundary, int a0, int a1, bool prev) {
+            double sum = 0;
+            int64_t n = 0;
+            for (int c = 0; c < g; ++c)
+                for (int64_t t = prev ? 1 : 0; t < k; ++t) {
+                    if (((t % tile) == 0) != boundary) continue;
+                    const unsigned long long* x = &h[(size_t)(t * g + c) * S];
+                    const unsigned long long* xp = prev ? &h[(size_t)((t - 1) * g + c) * S] : x;
+                    if (!xp[a0] || !x[a1]) continue;
+                    sum += double((long long)(x[a1] - xp[a0]));
+                    ++n;
+                }
+            return n ? sum / n : 0.0;
+        };
+        for (int bnd = 0; bnd < 2; ++bnd)
+            std::fprintf(stderr,
+                         "[plnmf] exchange trace, %s columns (SM cycles, mean over CTAs): arrive->complete %.0f, "
+                         "->read %.0f, ->xwarp past barrier %.0f, read->chain past barrier %.0f, ->value %.0f | "
+                         "prev value->square parked %.0f, ->xwarp has partial %.0f, ->arrive %.0f\n",
+                         bnd ? "tile-first" : "in-tile", span(bnd, 0, 1, false), span(bnd, 1, 2, false),
+                         span(bnd, 2, 3, false), span(bnd, 2, 4, false), span(bnd, 4, 5, false), span(bnd, 5, 6, true),
+                         span(bnd, 6, 7, false), span(bnd, 7, 0, false));
+        // tile boundaries: stamps 8..13 on each tile's last column
+        double bs[6] = {0, 0, 0, 0, 0, 0};
+        int64_t nb = 0;
+        for (int c = 0; c < g; ++c)
+            for (int64_t t = tile - 1; t + 1 < k; t += tile) {
+                const unsigned long long* x = &h[(size_t)(t * g + c) * S];
+                const unsigned long long* y = &h[(size_t)((t + 1) * g + c) * S];
+                const unsigned long long ev[7] = {x[5], x[8], x[9], x[10], x[11], x[12], x[13]};
+                for (int i = 0; i < 6; ++i) bs[i] += double((long long)(ev[i + 1] - ev[i]));
+                (void)y;
+                ++nb;
             }
-            poll += cp;
-            pmax = std::max(pmax, cp / k);
-        }
-        std::fprintf(stderr, "[plnmf] exchange trace (SM cycles/column, mean over CTAs): arrival->complete %.0f "
-                     "(max CTA %.0f), complete->partials read %.0f, read->next arrival %.0f\n",
-                     poll / k / g, pmax, read / k / g, gap / (k - 1) / g);
+        if (nb)
+            std::fprintf(stderr, "[plnmf] tile boundary (SM cycles): last value->publish start %.0f, ->publish done %.0f, "
+                         "->past __syncthreads %.0f, ->phase-3 done %.0f, ->coeff block + sync %.0f, ->first value %.0f\n",
+                         bs[0] / nb, bs[1] / nb, bs[2] / nb, bs[3] / nb, bs[4] / nb, bs[5] / nb);
     }
     return 1;
 }

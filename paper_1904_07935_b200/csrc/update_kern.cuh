@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             else lookahead_gemm_resident<M, 4>(ga, resid, p.ldr);
             return;
         }
-        if (TMAX > 0 && SQN && p.kc > 0 && count == nupd) {
+        if (TMAX > 0 && SQN && p.kc > 0 && count <= nupd) {
             gemm_next(dst, bn, en, bprev, count, self);
             return;
         }
@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         const int bn = e, en = min(e + T, k);
         const bool has_next = bn < k;
         double* A = acc[cur];
+        // PLNMF_TRACE_EXCHANGE: tile-boundary stamps go to the tile's last column
+        unsigned long long* const btr =
+            p.trace ? p.trace + ((int64_t)(e - 1) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
         if (is_chain && TMAX > 0 && NORMALIZE && kExactM<M>) {
             // ---- W phase 2, latency-ordered (Math::exact).  Everything that does
             // not depend on the column's norm is computed while the exchange is
@@ -357,29 +360,35 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     val = clamp_floor(p.eps, dsub(dadd(arow[0], add0), s));
                 }
             }
+            if (p.trace && b > 0 && ctid == 0) p.trace[((int64_t)(b - 1) * gridDim.x + blockIdx.x) * kTraceSlots + 13] = clock64();
+            // the additive term is read from global one column ahead of its use
+            // (an HBM/L2 load: ~1K cycles that the prefix would otherwise stall on)
+            double add_nx = (own && w > 1) ? addr[1] : 0.0;
             // not unrolled: one column's code (exchange included) stays resident
             // in the instruction cache across the whole update
 #pragma unroll 1
             for (int tt = 0; tt < w; ++tt) {
                 {
+                    unsigned long long* const trc =
+                        p.trace ? p.trace + ((int64_t)(b + tt) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
                     const bool more = tt + 1 < w;
                     if (!is_xwarp) {
                         const double ss = (p.dbg & 8) ? val : warp_sum_lane0(dmul(val, val));
                         if (lane_id() == 0) red[ctid >> 5] = ss;
                     }
                     mark(kProfDot);
+                    if (trc && ctid == 0) trc[6] = clock64();
                     named_sync(1, nchain);
                     double pre = 0.0, c1 = 0.0, u1 = 0.0;
                     if (is_xwarp) {
-                        double blk = 0.0;
-                        if (lane_id() == 0) {
-                            // fixed order over 8 slots; slots >= row_warps hold +0.0 (x + 0.0 == x)
-                            blk = red[0];
+                        // every lane adds the 8 warp partials in one fixed pairwise tree
+                        // (slots >= row_warps hold +0.0): no broadcast shuffle needed
+                        double v[8];
 #pragma unroll
-                            for (int i = 1; i < 8; ++i) blk = dadd(blk, red[i]);
-                        }
-                        blk = __shfl_sync(0xffffffffu, blk, 0);
+                        for (int i = 0; i < 8; ++i) v[i] = red[i];
+                        const double blk = tree8(v);
                         mark(kProfChain);
+                        if (trc && lane_id() == 0) trc[7] = clock64();
                         const double norm = (p.dbg & 32) ? __dsqrt_rn(blk)
                                                          : grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters,
                                                                          p.trace);
@@ -403,10 +412,12 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         for (int j = 0; j < TM; ++j)
                             if (j > tt && j < w) prod[j * R] = dmul(orow[j], sqc[j * T + tt + 1]);
                         c1 = sqc[tt * T + tt + 1];
-                        u1 = dadd(arow[tt + 1], addr[tt + 1]);  // L2 latency hidden by the exchange
+                        u1 = dadd(arow[tt + 1], add_nx);
+                        if (tt + 2 < w) add_nx = addr[tt + 2];  // consumed by the next column's prefix
                         mark(kProfUpd);
                     }
                     named_sync(1, nchain);
+                    if (trc && (ctid == 0 || ctid == nrowt)) trc[ctid == 0 ? 4 : 3] = clock64();
                     double nv;  // max(eps, val / norm), tiled.cpp:146
                     {
                         const double bn = red[40], y = red[41];
@@ -414,7 +425,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                             const double q0 = __dmul_rn(val, y);
                             nv = clamp_floor(p.eps, __fma_rn(__fma_rn(-q0, bn, val), y, q0));
                         } else {
-                            nv = clamp_floor(p.eps, __ddiv_rn(val, bn));
+                            nv = clamp_floor(p.eps, div_outlined(val, bn));
                         }
                     }
                     if (own) {
@@ -429,6 +440,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         }
                     }
                     mark(kProfDiv);
+                    if (trc && ctid == 0) trc[5] = clock64();
                 }
             }
             named_sync(1, nchain);
@@ -569,6 +581,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             }
             // publish the finished tile (rows were thread-private until here)
             named_sync(1, nchain);
+            if (btr && ctid == 0) btr[8] = clock64();
             for (int idx = ctid; idx < nrows * w; idx += nchain) {
                 const int r = idx / w, j = idx % w;
                 p.out[(r0 + r) * k + b + j] = A[r * ldt + j];
@@ -582,11 +595,16 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             cp_async_wait<0>();
             named_sync(2, nupd);
 #ifndef PLNMF_CHAIN_ONLY  // timing experiment: the chain with the look-ahead compiled out
-            if (p.overlap != 2) build_next(acc[cur ^ 1], bn, en, b, 0, nupd, utid);  // 2: timing probe only
+            {
+                const int nla = (p.dbg >> 8) ? min((p.dbg >> 8) * kWarp, nupd) : nupd;
+                if (p.overlap != 2 && utid < nla) build_next(acc[cur ^ 1], bn, en, b, 0, nla, utid);  // 2: timing probe only
+            }
 #endif
             mark(kProfUpd);
         }
+        if (btr && tid == nupd) btr[9] = clock64();
         __syncthreads();
+        if (btr && tid == nupd) btr[10] = clock64();
         mark(kProfWait);
 #ifndef PLNMF_CHAIN_ONLY
         if (has_next && !p.overlap) {
@@ -618,8 +636,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     if (u < wq) An[r * ldt + cq + u] = a[u];
             }
 #endif
+            if (btr && tid == nupd) btr[11] = clock64();
             load_sqc(bn, en, tid, kLThreads);
             __syncthreads();
+            if (btr && tid == nupd) btr[12] = clock64();
             mark(kProfBoundary);
         }
         cur ^= 1;
