@@ -86,8 +86,31 @@ def test_tiled_updates_20news_scale(gpu, tile):
     p, q = eng.get_product("p"), eng.get_product("q")
     eng.update_w(cfg, A.tiled)
     w1, norms = R.update_tiled(f.w, q, p, tile, is_w=True)
-    assert rel_max(w1, eng.get_factors().w) <= 1e-12
+    w_eng = eng.get_factors().w
+    assert rel_max(w1, w_eng) <= 1e-12
     assert elem_rel(norms, eng.get_product("column_norms")) <= 1e-12
+    # the next iteration's R = A^T W from the engine's new W
+    eng.precompute_h_products()
+    trp, tci, tval = ref_at(m)
+    assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, w_eng))
+
+
+@pytest.mark.parametrize("k,tile", [(50, 7), (33, 32), (8, 8), (1, 1)])
+def test_step_api_r_after_w_update_bitwise(gpu, k, tile):
+    """Through the step API, R = A^T W_new after each tiled W update (ragged
+    last tile, a single tile, K=1) equals spmm_into of the engine's own new W
+    bit for bit, over two whole iterations."""
+    m, eng, f = make(3000, 1700, 0.01, k)
+    cfg = P.SolverConfig(rank=k, tile_size=tile)
+    trp, tci, tval = ref_at(m)
+    for _ in range(2):
+        eng.precompute_h_products()
+        eng.update_h(cfg, A.tiled)
+        eng.precompute_w_products()
+        eng.update_w(cfg, A.tiled)
+        eng.precompute_h_products()
+        w = eng.get_factors().w
+        assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, w))
 
 
 def _well_conditioned_state(m, k, iters=3, tile=0):
