@@ -113,6 +113,42 @@ def test_step_api_r_after_w_update_bitwise(gpu, k, tile):
         assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, w))
 
 
+@pytest.mark.parametrize("k,tile", [(24, 5), (40, 16), (9, 9)])
+def test_streaming_fallback_updates(gpu, k, tile, monkeypatch):
+    """The streaming tiled update (stream.cu: phase A + one persistent
+    streaming launch; the planner's choice when one SM's rows do not fit the
+    persistent kernel, e.g. C5), forced on a small instance: H bitwise, W to
+    1e-12 (norm reduction order only)."""
+    monkeypatch.setenv("PLNMF_FORCE_STREAMING", "1")
+    m, eng, f = make(2500, 1300, 0.01, k)
+    eng.precompute_h_products()
+    r, s = eng.get_product("r"), eng.get_product("s")
+    cfg = P.SolverConfig(rank=k, tile_size=tile)
+    eng.update_h(cfg, A.tiled)
+    ht1, _ = R.update_tiled(f.ht, s, r, tile, is_w=False)
+    assert bits_equal(eng.get_factors().ht, ht1)
+    eng.precompute_w_products()
+    p, q = eng.get_product("p"), eng.get_product("q")
+    eng.update_w(cfg, A.tiled)
+    w1, norms = R.update_tiled(f.w, q, p, tile, is_w=True)
+    assert rel_max(w1, eng.get_factors().w) <= 1e-12
+    assert elem_rel(norms, eng.get_product("column_norms")) <= 1e-12
+
+
+def test_streaming_chosen_for_tall_w(gpu):
+    """More W rows than 256 per SM: the planner streams the W update on its
+    own (no override); still within 1e-12 of the oracle."""
+    k, tile = 8, 3
+    m, eng, f = make(40000, 300, 0.02, k)
+    cfg = P.SolverConfig(rank=k, tile_size=tile)
+    eng.precompute_w_products()
+    p, q = eng.get_product("p"), eng.get_product("q")
+    eng.update_w(cfg, A.tiled)
+    w1, norms = R.update_tiled(f.w, q, p, tile, is_w=True)
+    assert rel_max(w1, eng.get_factors().w) <= 1e-12
+    assert elem_rel(norms, eng.get_product("column_norms")) <= 1e-12
+
+
 def _well_conditioned_state(m, k, iters=3, tile=0):
     """Oracle fast-hals trajectory from the seed, to move past the collapse
     of iteration 1 (Finding 1)."""
