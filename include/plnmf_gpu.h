@@ -238,6 +238,15 @@ plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* c
  * *avg_ms = mean CUDA-event duration per launch (events on the engine stream). */
 plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg, int32_t which,
                                    int32_t reps, double* avg_ms);
+/* GPU tile selection, replacing best_integer_tile's cache model
+ * (proj/include/plnmf/cost_model.hpp:65, proj/src/cost_model.cpp:131-142):
+ * times one tiled H + W update from the current factors for each candidate
+ * T (n == 0: 1, 2, 4, 8, 12, 16, 20, 24, 32 up to K), restores the factors,
+ * and returns the fastest T in *best; update_ms[i] (optional, n entries, or 9
+ * when n == 0) gets each candidate's time.  Results are parity-neutral: every
+ * T reproduces the reference's tiled update for that T. */
+plnmf_status plnmf_gpu_best_integer_tile(plnmf_gpu_engine* e, const plnmf_config* cfg, const int32_t* candidates,
+                                         int32_t n, int32_t* best, double* update_ms);
 plnmf_status plnmf_gpu_get_stats(const plnmf_gpu_engine* e, plnmf_gpu_stats* out);
 plnmf_status plnmf_gpu_synchronize(plnmf_gpu_engine* e);
 

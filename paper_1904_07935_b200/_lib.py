@@ -83,6 +83,8 @@ SIGNATURES = {
     "plnmf_gpu_local_pw": (C.c_int, [Engine_p, P_f64]),
     "plnmf_gpu_run_iterations": (C.c_int, [Engine_p, P_cfg, C.c_int, i64, P_f64]),
     "plnmf_gpu_time_kernel": (C.c_int, [Engine_p, P_cfg, i32, i32, P_f64]),
+    "plnmf_gpu_best_integer_tile": (C.c_int, [Engine_p, P_cfg, C.POINTER(C.c_int32), i32, C.POINTER(C.c_int32),
+                                              P_f64]),
     "plnmf_gpu_get_stats": (C.c_int, [Engine_p, C.POINTER(StatsC)]),
     "plnmf_gpu_synchronize": (C.c_int, [Engine_p]),
 }

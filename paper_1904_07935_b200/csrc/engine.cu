@@ -1010,6 +1010,81 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
     });
 }
 
+// GPU tile selection: the reference picks T from a cache
+// model (best_integer_tile, proj/src/cost_model.cpp:131-142); on the GPU the
+// update kernels' cost is set by their shared-memory staging and register-tile
+// instantiations (T <= 16 / <= 32), not by a 35 MB cache, so the candidates are
+// measured: for each T, one warm-up and one timed H + W tiled update from the
+// current factors (products recomputed per T), factors restored afterwards.
+plnmf_status plnmf_gpu_best_integer_tile(plnmf_gpu_engine* e, const plnmf_config* cfg, const int32_t* candidates,
+                                         int32_t n, int32_t* best, double* update_ms) {
+    return guarded([&] {
+        check_engine(e);
+        if (!cfg || !best || n < 0 || (n > 0 && !candidates))
+            throw std::invalid_argument("best_integer_tile: bad argument");
+        if (e->shard) throw std::invalid_argument("best_integer_tile: not available on a shard engine");
+        plnmf::validate_config(*cfg);
+        if (cfg->rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
+        std::vector<int32_t> cand;
+        if (n > 0) {
+            cand.assign(candidates, candidates + n);
+        } else {
+            for (int32_t t : {1, 2, 4, 8, 12, 16, 20, 24, 32})
+                if (t <= e->k) cand.push_back(t);
+        }
+        for (int32_t t : cand)
+            if (t < 1 || t > e->k) throw std::invalid_argument("best_integer_tile: tile size must be in [1, K]");
+        double *w0 = nullptr, *h0 = nullptr;
+        const size_t wb = sizeof(double) * (size_t)(e->v * e->k), hb = sizeof(double) * (size_t)(e->d * e->k);
+        PLNMF_CUDA_CHECK(cudaMalloc(&w0, wb));
+        PLNMF_CUDA_CHECK(cudaMalloc(&h0, hb));
+        auto restore = [&] {
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->w, w0, wb, cudaMemcpyDeviceToDevice, e->s));
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->ht, h0, hb, cudaMemcpyDeviceToDevice, e->s));
+            e->s_valid = false;
+            e->r_valid = false;
+        };
+        try {
+            PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(w0, e->w, wb, cudaMemcpyDeviceToDevice, e->s));
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(h0, e->ht, hb, cudaMemcpyDeviceToDevice, e->s));
+            cudaEvent_t a0 = event_at(e, 0), a1 = event_at(e, 1), b0 = event_at(e, 2), b1 = event_at(e, 3);
+            double best_ms = 0.0;
+            for (size_t i = 0; i < cand.size(); ++i) {
+                plnmf_config c = *cfg;
+                c.tile_size = cand[i];
+                double ms = 0.0;
+                for (int rep = 0; rep < 2; ++rep) {  // warm-up (plans, coefficient panels), then timed
+                    restore();
+                    precompute_h(e);
+                    PLNMF_CUDA_CHECK(cudaEventRecord(a0, e->s));
+                    update_h(e, c, PLNMF_ALGORITHM_TILED);
+                    PLNMF_CUDA_CHECK(cudaEventRecord(a1, e->s));
+                    precompute_w(e);
+                    PLNMF_CUDA_CHECK(cudaEventRecord(b0, e->s));
+                    update_w(e, c, PLNMF_ALGORITHM_TILED);
+                    PLNMF_CUDA_CHECK(cudaEventRecord(b1, e->s));
+                    PLNMF_CUDA_CHECK(cudaEventSynchronize(b1));
+                    ms = (elapsed_s(a0, a1) + elapsed_s(b0, b1)) * 1e3;
+                }
+                if (update_ms) update_ms[i] = ms;
+                if (i == 0 || ms < best_ms) {
+                    best_ms = ms;
+                    *best = cand[i];
+                }
+            }
+            restore();
+            PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        } catch (...) {
+            cudaFree(w0);
+            cudaFree(h0);
+            throw;
+        }
+        PLNMF_CUDA_CHECK(cudaFree(w0));
+        PLNMF_CUDA_CHECK(cudaFree(h0));
+    });
+}
+
 plnmf_status plnmf_gpu_get_stats(const plnmf_gpu_engine* e, plnmf_gpu_stats* out) {
     return guarded([&] {
         if (!e || !out) throw std::invalid_argument("plnmf_gpu_get_stats: null argument");

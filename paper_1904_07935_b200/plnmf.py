@@ -384,6 +384,21 @@ class Engine:
         _check(L.lib().plnmf_gpu_run_iterations(self._h, C.byref(c), int(algorithm), n, C.byref(ms)))
         return ms.value
 
+    def best_integer_tile(self, config: SolverConfig, candidates=None):
+        """GPU counterpart of best_integer_tile (proj/src/cost_model.cpp:131-142):
+        the candidate T whose tiled H + W update from the current factors is
+        fastest on this device (measured; the factors are left unchanged).
+        Returns (best T, {T: update ms})."""
+        c = config.to_c()
+        cand = list(candidates) if candidates else []
+        arr = (C.c_int32 * max(1, len(cand)))(*cand)
+        times = (C.c_double * max(9, len(cand)))()
+        best = C.c_int32()
+        _check(L.lib().plnmf_gpu_best_integer_tile(self._h, C.byref(c), arr, len(cand), C.byref(best), times))
+        if not cand:
+            cand = [t for t in (1, 2, 4, 8, 12, 16, 20, 24, 32) if t <= config.rank]
+        return best.value, {t: times[i] for i, t in enumerate(cand)}
+
     def time_kernel(self, config: SolverConfig, which: int, reps: int) -> float:
         c = config.to_c()
         ms = C.c_double()

@@ -149,6 +149,24 @@ def test_streaming_chosen_for_tall_w(gpu):
     assert elem_rel(norms, eng.get_product("column_norms")) <= 1e-12
 
 
+def test_best_integer_tile_measures_and_restores(gpu):
+    """The GPU tile selector (f3) returns one of the candidates, times each,
+    and leaves the factors exactly as they were."""
+    k = 40
+    m, eng, f = make(3000, 1700, 0.01, k)
+    before = eng.get_factors()
+    cfg = P.SolverConfig(rank=k)
+    best, times = eng.best_integer_tile(cfg, [4, 8, 16, 40])
+    assert best in (4, 8, 16, 40) and set(times) == {4, 8, 16, 40}
+    assert all(t > 0 for t in times.values()) and times[best] == min(times.values())
+    after = eng.get_factors()
+    assert bits_equal(after.w, before.w) and bits_equal(after.ht, before.ht)
+    best_default, times_default = eng.best_integer_tile(cfg)
+    assert best_default in times_default and max(times_default) <= k
+    with pytest.raises(ValueError):
+        eng.best_integer_tile(cfg, [0])
+
+
 def _well_conditioned_state(m, k, iters=3, tile=0):
     """Oracle fast-hals trajectory from the seed, to move past the collapse
     of iteration 1 (Finding 1)."""
