@@ -596,6 +596,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             named_sync(2, nupd);
 #ifndef PLNMF_CHAIN_ONLY  // timing experiment: the chain with the look-ahead compiled out
             {
+                // PLNMF_DBG >> 8: look-ahead width in warps (timing experiments only; 0 = all)
                 const int nla = (p.dbg >> 8) ? min((p.dbg >> 8) * kWarp, nupd) : nupd;
                 if (p.overlap != 2 && utid < nla) build_next(acc[cur ^ 1], bn, en, b, 0, nla, utid);  // 2: timing probe only
             }
