@@ -319,22 +319,24 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                          bnd ? "tile-first" : "in-tile", span(bnd, 0, 1, false), span(bnd, 1, 2, false),
                          span(bnd, 2, 3, false), span(bnd, 2, 4, false), span(bnd, 4, 5, false), span(bnd, 5, 6, true),
                          span(bnd, 6, 7, false), span(bnd, 7, 0, false));
-        // tile boundaries: stamps 8..13 on each tile's last column
-        double bs[6] = {0, 0, 0, 0, 0, 0};
+        // tile boundaries: stamps 9..13 on each tile's last column (chain warp 0; the exact
+        // W path publishes without a stamp of its own, so the first span includes the publish)
+        double bs[5] = {0, 0, 0, 0, 0};
         int64_t nb = 0;
         for (int c = 0; c < g; ++c)
             for (int64_t t = tile - 1; t + 1 < k; t += tile) {
                 const unsigned long long* x = &h[(size_t)(t * g + c) * S];
-                const unsigned long long* y = &h[(size_t)((t + 1) * g + c) * S];
-                const unsigned long long ev[7] = {x[5], x[8], x[9], x[10], x[11], x[12], x[13]};
-                for (int i = 0; i < 6; ++i) bs[i] += double((long long)(ev[i + 1] - ev[i]));
-                (void)y;
+                const unsigned long long ev[6] = {x[5], x[9], x[10], x[11], x[12], x[13]};
+                bool ok = true;
+                for (int i = 0; i < 6; ++i) ok = ok && ev[i] != 0;
+                if (!ok) continue;
+                for (int i = 0; i < 5; ++i) bs[i] += double((long long)(ev[i + 1] - ev[i]));
                 ++nb;
             }
         if (nb)
-            std::fprintf(stderr, "[plnmf] tile boundary (SM cycles): last value->publish start %.0f, ->publish done %.0f, "
-                         "->past __syncthreads %.0f, ->phase-3 done %.0f, ->coeff block + sync %.0f, ->first value %.0f\n",
-                         bs[0] / nb, bs[1] / nb, bs[2] / nb, bs[3] / nb, bs[4] / nb, bs[5] / nb);
+            std::fprintf(stderr, "[plnmf] tile boundary (SM cycles): last value->published %.0f, ->past __syncthreads %.0f, "
+                         "->phase-3 done %.0f, ->coeff block + sync %.0f, ->first value %.0f\n",
+                         bs[0] / nb, bs[1] / nb, bs[2] / nb, bs[3] / nb, bs[4] / nb);
     }
     return 1;
 }
