@@ -444,10 +444,15 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 }
             }
             named_sync(1, nchain);
-            for (int idx = ctid; idx < nrows * w; idx += nchain) {
-                const int rr = idx / w, j = idx % w;
-                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
-                if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
+            if (w == 16 && !p.resident) {  // full 16-wide tiles: shifts instead of a runtime division
+                for (int idx = ctid; idx < nrows * 16; idx += nchain)
+                    p.out[(r0 + (idx >> 4)) * k + b + (idx & 15)] = A[(idx >> 4) * ldt + (idx & 15)];
+            } else {
+                for (int idx = ctid; idx < nrows * w; idx += nchain) {
+                    const int rr = idx / w, j = idx % w;
+                    p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+                    if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
+                }
             }
             mark(kProfChain);
         } else if (is_chain && TMAX > 0) {
@@ -623,8 +628,23 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             double* An = acc[cur ^ 1];
             const int wn = en - bn;
 #ifndef PLNMF_CHAIN_ONLY
+            if (TMAX > 0 && SQN) {
+                // zero-padded staged panel: 8-wide register rows (row_panel, the same per-element
+                // madd sequence as accumulate_quad), one item per thread for 16-wide tiles
+                const int n8 = (wn + 7) / 8;
+                for (int item = tid; item < nrows * n8; item += kLThreads) {
+                    const int r = item / n8, c8 = (item % n8) * 8;
+                    double a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = (c8 + u < wn) ? An[r * ldt + c8 + u] : 0.0;
+                    row_panel<M, 8>(a, A + r * ldt - b, b, e, Qn(bn), TQ, c8);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c8 + u < wn) An[r * ldt + c8 + u] = a[u];
+                }
+            }
             const int nq = (wn + kLQuad - 1) / kLQuad;
-            for (int item = tid; item < nrows * nq; item += kLThreads) {
+            for (int item = tid; item < ((TMAX > 0 && SQN) ? 0 : nrows * nq); item += kLThreads) {
                 const int r = item / nq, cq = (item % nq) * kLQuad;
                 const int wq = min(kLQuad, wn - cq);
                 double a[kLQuad];
