@@ -291,6 +291,23 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         cp_async_commit();
     };
 
+    // exact W chain with a concurrent look-ahead: a finished tile (all T columns; only the
+    // last tile may be narrower) is published to global by the look-ahead warps at the start
+    // of the next tile, before build_next reuses its buffer, instead of by the chain at the
+    // tile boundary
+    const bool la_pub = NORMALIZE && kExactM<M> && TMAX > 0 && p.overlap == 1 && !p.resident;
+    auto publish_prev = [&](const double* P, int pb) {
+        if (T == 16) {
+            for (int idx = utid; idx < nrows * 16; idx += nupd)
+                p.out[(r0 + (idx >> 4)) * k + pb + (idx & 15)] = P[(idx >> 4) * ldt + (idx & 15)];
+        } else {
+            for (int idx = utid; idx < nrows * T; idx += nupd) {
+                const int rr = idx / T, j = idx % T;
+                p.out[(r0 + rr) * k + pb + j] = P[rr * ldt + j];
+            }
+        }
+    };
+
     // ---- prologue: tile 0 accumulators (init + phase 1), coeff blocks, tile-0 operands
     {
         const int e0 = min(T, k);
@@ -444,7 +461,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 }
             }
             named_sync(1, nchain);
-            if (w == 16 && !p.resident) {  // full 16-wide tiles: shifts instead of a runtime division
+            if (la_pub && has_next) {
+                // published by the look-ahead warps at the start of the next tile
+            } else if (w == 16 && !p.resident) {  // full 16-wide tiles: shifts instead of a runtime division
                 for (int idx = ctid; idx < nrows * 16; idx += nchain)
                     p.out[(r0 + (idx >> 4)) * k + b + (idx & 15)] = A[(idx >> 4) * ldt + (idx & 15)];
             } else {
@@ -595,6 +614,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             mark(kProfChain);
         } else if (has_next && p.overlap) {
             // ---- look-ahead: next tile's accumulators, minus this tile's phase-3 term
+            if (la_pub && b > 0) publish_prev(acc[cur ^ 1], b - T);  // before build_next reuses it
             load_sqn(bn, en, utid, nupd);
             stage_tile(cur ^ 1, bn, en, utid, nupd);
             cp_async_wait<0>();
@@ -607,6 +627,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             }
 #endif
             mark(kProfUpd);
+        } else if (la_pub && !is_chain && b > 0) {
+            publish_prev(acc[cur ^ 1], b - T);  // last tile: only the previous tile is left to publish
         }
         if (btr && tid == nupd) btr[9] = clock64();
         __syncthreads();
