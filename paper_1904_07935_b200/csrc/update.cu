@@ -73,7 +73,7 @@ int64_t pl_kbuf(int64_t rows, int64_t k, int64_t tile, bool normalize) {
 size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem, int kc, int kst = 2,
                bool normalize = false) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
-    const int64_t prods = (normalize && tile <= 32) ? rows * tile : 0;  // W chain products (exact path)
+    const int64_t prods = (normalize && tile <= 32) ? rows * (tile + 1) : 0;  // W chain products (exact path)
     const int64_t rings = kc > 0 ? kst * pl_kbuf(rows, k, tile, normalize) * (kc + 2) : 0;
     return sizeof(double) * (size_t)((stage_ops ? 4 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
                                      tile * tile + 48 + 1 + rings + prods);

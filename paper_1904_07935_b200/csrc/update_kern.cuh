@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             constexpr int TM = TMAX > 0 ? TMAX : 1;
             const int r = ctid;
             const bool own = !is_xwarp && r < nrows;
-            double* prod = prodS + r;  // prod[j * R]: this row's products, conflict-free across lanes
+            // prod[j]: this row's products at a row stride of T + 1 doubles (odd: lanes' 64-bit
+            // accesses spread over the banks), so every j is an immediate offset from one base
+            double* prod = prodS + r * (T + 1);
             double* arow = A + r * ldt;
             const double* addr = p.add + (r0 + r) * k + b;
             const double* orow = p.resident ? resid + r * p.ldr + b
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                             if (j < tt) pre = dadd(pre, dmul(arow[j], sqc[j * T + tt + 1]));
 #pragma unroll
                         for (int j = 0; j < TM; ++j)
-                            if (j > tt && j < w) prod[j * R] = dmul(orow[j], sqc[j * T + tt + 1]);
+                            if (j > tt && j < w) prod[j] = dmul(orow[j], sqc[j * T + tt + 1]);
                         c1 = sqc[tt * T + tt + 1];
                         u1 = dadd(arow[tt + 1], add_nx);
                         if (tt + 2 < w) add_nx = addr[tt + 2];  // consumed by the next column's prefix
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                             if (!(p.dbg & 2))
 #pragma unroll
                                 for (int j = 0; j < TM; ++j)
-                                    if (j > tt && j < w) s2 = dadd(s2, prod[j * R]);
+                                    if (j > tt && j < w) s2 = dadd(s2, prod[j]);
                             val = clamp_floor(p.eps, dsub(u1, s2));
                         }
                     }
