@@ -49,7 +49,20 @@ typedef enum plnmf_algorithm { PLNMF_ALGORITHM_REFERENCE = 0, PLNMF_ALGORITHM_TI
  * separately, round-to-nearest, in the reference's per-element order (no FMA
  * contraction — the reference Release build has none).  FUSED uses fma() in
  * the same order (one rounding per multiply-add). */
-typedef enum plnmf_math { PLNMF_MATH_EXACT = 0, PLNMF_MATH_FUSED = 1 } plnmf_math;
+typedef enum plnmf_math {
+    PLNMF_MATH_EXACT = 0,
+    PLNMF_MATH_FUSED = 1,
+    /* Verification mode: EXACT arithmetic plus the
+     * reference's own summation order for the two reductions the fast path
+     * forms as fixed trees — the W column norms (serial over the rows for
+     * fast-hals, proj/src/hals.cpp:97-100; per-OpenMP-thread chunk partials
+     * combined in thread order for pl-nmf, proj/src/tiled.cpp:103-142, with
+     * the team size set by plnmf_gpu_set_reference_threads) and the
+     * Gram-identity dots <P,W>, <S,Q> (serial, proj/src/metrics.cpp:104-115).
+     * With it, iterate() trajectories are bit-identical to the reference's.
+     * Column-stepped and slow (serial chains): not the production path. */
+    PLNMF_MATH_REFERENCE_ORDER = 2
+} plnmf_math;
 
 /* proj/include/plnmf/config.hpp:11-22 — SolverConfig, field for field. */
 typedef struct plnmf_config {
@@ -146,6 +159,10 @@ plnmf_status plnmf_gpu_destroy(plnmf_gpu_engine* e);
 plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int64_t* cols,
                                   int64_t* nnz, double* norm_sq);
 plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math);
+/* PLNMF_MATH_REFERENCE_ORDER only: the reference's OpenMP team size
+ * (omp_get_max_threads(), `--threads`, proj/tools/plnmf.cpp:104-106), which
+ * fixes its tiled norm partials (tiled.cpp:97-99).  Default 1. */
+plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthreads);
 
 /* FactorPair in/out (proj/include/plnmf/workspace.hpp:32-35). */
 plnmf_status plnmf_gpu_set_factors(plnmf_gpu_engine* e, const double* w_colmajor,

@@ -54,7 +54,21 @@ _ORA_SIGS = {
     "ora_relative_error_direct_csr": (None, [i64, i64, P_i64, P_i64, P_f64, f64, i64, P_f64, P_f64, P_f64]),
     "ora_norm_sq": (f64, [i64, P_f64]),
     "ora_factor_deviation": (f64, [i64, P_f64, P_f64]),
+    "ora_synth_csr": (cint, [i64, i64, f64, u64, P_i64, P_i64, P_f64, P_i64]),
 }
+
+
+def synth_csr(rows, cols, density, seed=20):
+    """The SURVEY.md 8(d) synthetic CSR (oracle/synth.c, the same stream as the
+    engine's plnmf_synth_csr) as (row_ptr, col_idx, values) int64/int64/f64."""
+    rp = np.zeros(rows + 1, np.int64)
+    nnz = C.c_int64()
+    if ora().ora_synth_csr(rows, cols, density, seed, i64p(rp), None, None, C.byref(nnz)):
+        raise ValueError("synth_csr: bad arguments")
+    ci = np.zeros(nnz.value, np.int64)
+    val = np.zeros(nnz.value)
+    ora().ora_synth_csr(rows, cols, density, seed, i64p(rp), i64p(ci), f64p(val), C.byref(nnz))
+    return rp, ci, val
 
 
 def ora():

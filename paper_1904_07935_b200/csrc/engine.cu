@@ -33,6 +33,10 @@ struct plnmf_gpu_engine {
     bool sparse = true;
     double a2 = 0.0;
     Math math = Math::exact;
+    // Math::reference_order (PLNMF_MATH_REFERENCE_ORDER): exact arithmetic plus the
+    // reference's own summation order for the W norms and the error dots (refmode.cu)
+    bool ref_order = false;
+    int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
 
     int64_t *rp = nullptr, *trp = nullptr;
     int32_t *ci = nullptr, *tci = nullptr;
@@ -291,7 +295,45 @@ void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
     }
 }
 
+// The W update with the reference's norm order (Math::reference_order): column
+// stepped, one launch per piece.  Tiled: phase A (init + phase 1), then per
+// column the phase-2 values (the fast path's per-element order), the norm from
+// ref_threads chunk partials (tiled.cpp:103-142), the normalisation, and per tile
+// phase 3.  Fast-hals: per column the values and one serial norm (hals.cpp:87-103).
+void update_w_reference_order(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    if (!e->col_ss) e->col_ss = dalloc<double>(e, 1);
+    if (!e->col_partials) e->col_partials = dalloc<double>(e, 512);
+    const int64_t v = e->v, k = e->k;
+    if (alg == PLNMF_ALGORITHM_TILED) {
+        check_tile(cfg, k);
+        const int64_t T = cfg.tile_size;
+        e->launches += kern::stream_phase_a(e->s, Math::exact, v, k, T, true, e->w, e->q, e->w_new);
+        for (int64_t b = 0; b < k; b += T) {
+            const int64_t en = std::min(k, b + T);
+            for (int64_t t = b; t < en; ++t) {
+                e->launches += kern::shard_col_step(e->s, Math::exact, v, k, b, en, t, cfg.epsilon, e->w, e->w_new,
+                                                    e->q, e->p, e->col_partials, nullptr);
+                e->launches += kern::ordered_ss(e->s, v, k, t, e->ref_threads, e->w_new, e->col_ss);
+                e->launches += kern::shard_normalize(e->s, v, k, t, cfg.epsilon, 1, e->col_ss, e->w_new, e->norms);
+            }
+            e->launches += kern::shard_phase3(e->s, Math::exact, v, k, b, en, e->w_new, e->q);
+        }
+        std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
+        e->update_macs += tiled_macs(v, k, T, true);
+    } else {
+        for (int64_t kk = 0; kk < k; ++kk) {
+            e->launches += kern::ref_w_values(e->s, v, k, kk, cfg.epsilon, e->w, e->p, e->q);
+            e->launches += kern::ordered_ss(e->s, v, k, kk, 1, e->w, e->col_ss);
+            e->launches += kern::shard_normalize(e->s, v, k, kk, cfg.epsilon, 1, e->col_ss, e->w, e->norms);
+        }
+        e->update_macs += (uint64_t)v * k * (k + 3);
+    }
+    e->s_valid = false;
+    e->r_valid = false;
+}
+
 void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    if (e->ref_order && !e->shard) return update_w_reference_order(e, cfg, alg);
     if (alg == PLNMF_ALGORITHM_TILED) {
         check_tile(cfg, e->k);
         ensure_plans(e, cfg.tile_size);
@@ -355,8 +397,13 @@ ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
         e->r_valid = true;
     }
-    e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
-    e->launches += kern::dot(e->s, e->math, e->k * e->k, e->sm, e->q, e->dot_partials, e->scalars + 1);
+    if (e->ref_order) {  // the reference's serial sums (metrics.cpp:104-115)
+        e->launches += kern::serial_dot_colmajor(e->s, e->v, e->k, e->p, e->w, e->scalars + 0);
+        e->launches += kern::serial_dot_colmajor(e->s, e->k, e->k, e->sm, e->q, e->scalars + 1);
+    } else {
+        e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
+        e->launches += kern::dot(e->s, e->math, e->k * e->k, e->sm, e->q, e->dot_partials, e->scalars + 1);
+    }
     e->launches += kern::error_finalize(e->s, e->a2, e->scalars + 0, e->scalars + 1, e->scalars + 2);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 2, e->scalars + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->s));
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
@@ -635,10 +682,21 @@ plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int6
 plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
     return guarded([&] {
         check_engine(e);
-        if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED) throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
-        e->math = math == PLNMF_MATH_EXACT ? Math::exact : Math::fused;
+        if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED && math != PLNMF_MATH_REFERENCE_ORDER)
+            throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
+        e->math = math == PLNMF_MATH_FUSED ? Math::fused : Math::exact;
+        e->ref_order = math == PLNMF_MATH_REFERENCE_ORDER;
         e->s_valid = false;
-    e->r_valid = false;
+        e->r_valid = false;
+    });
+}
+
+plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthreads) {
+    return guarded([&] {
+        check_engine(e);
+        if (nthreads < 1 || nthreads > 1024)
+            throw std::invalid_argument("plnmf_gpu_set_reference_threads: thread count must be in [1, 1024]");
+        e->ref_threads = nthreads;
     });
 }
 

@@ -102,6 +102,18 @@ int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v
                        double eps, double* w, const double* p, const double* q, double* norms,
                        double* partials, unsigned* counters, double* totals);
 
+// ---- reference-order reductions (Math::reference_order, refmode.cu) -------------------
+// *ss_out := column t's sum of squares of col_src (row-major n x k) in the
+// reference's order: nth = 1 serial (hals.cpp:97-100), nth > 1 per-thread
+// chunk partials added in thread order (tiled.cpp:103-106,129-142).
+int ordered_ss(cudaStream_t s, int64_t n, int64_t k, int64_t t, int nth, const double* col_src, double* ss_out);
+// column kk of update_w_reference before its normalisation (hals.cpp:88-96).
+int ref_w_values(cudaStream_t s, int64_t v, int64_t k, int64_t kk, double eps, double* w, const double* p,
+                 const double* q);
+// *out := serial sum of a.*b over the column-major order of row-major rows x cols
+// matrices (relative_error_gram, metrics.cpp:104-115).
+int serial_dot_colmajor(cudaStream_t s, int64_t rows, int64_t cols, const double* a, const double* b, double* out);
+
 // ---- metrics ---------------------------------------------------------------------
 // out := sum_i a[i]*b[i] (n elements), fixed-order two-pass reduction.
 constexpr int kDotBlocks = 296;

@@ -124,6 +124,7 @@ int shard_col_step(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t b, int6
         col_step_kernel<MathFused><<<grid, kColThreads, 0, s>>>(n, (int)k, (int)b, (int)e, (int)t, eps, old_m, nb,
                                                                 coeff, add, block_partials);
     PLNMF_CUDA_CHECK(cudaGetLastError());
+    if (!ss_out) return 1;  // reference-order mode forms the sum itself (refmode.cu)
     sum_fixed_kernel<<<1, 256, 0, s>>>((int)grid, block_partials, ss_out);
     PLNMF_CUDA_CHECK(cudaGetLastError());
     return 2;

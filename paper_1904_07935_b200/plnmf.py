@@ -76,6 +76,7 @@ class Algorithm(enum.IntEnum):
 class Math(enum.IntEnum):
     exact = 0  # separate rn multiply/add in the reference's order (bitwise where the order is shared)
     fused = 1  # fma in the same order
+    reference_order = 2  # exact + the reference's own W-norm and error-dot order (bitwise trajectories)
 
 
 @dataclass
@@ -312,6 +313,11 @@ class Engine:
 
     def set_math(self, math: Math) -> None:
         _check(L.lib().plnmf_gpu_set_math(self._h, int(math)))
+
+    def set_reference_threads(self, n: int) -> None:
+        """Math.reference_order: the reference's OpenMP team size (its tiled
+        norm partials depend on it, proj/src/tiled.cpp:97-99)."""
+        _check(L.lib().plnmf_gpu_set_reference_threads(self._h, int(n)))
 
     # ---- factors
     def set_factors(self, f: FactorPair) -> None:

@@ -124,3 +124,13 @@ def test_kat_macs_parity_formula():
                     m += n * wdt * b + n * wdt * wdt + (2 * n * wdt if is_w else 0) + n * wdt * (k - e)
                 tiled += m
             assert tiled == ref
+
+
+@pytest.mark.parametrize("rows,cols,density,seed", [(0, 5, 0.5, 1), (1, 1, 1.0, 2), (300, 200, 0.05, 20),
+                                                    (5000, 3000, 0.003, 7), (64, 50, 1.0, 3)])
+def test_oracle_generator_matches_engine_generator(rows, cols, density, seed):
+    """oracle/synth.c (used by bench.py's reference arm so that it never loads
+    the engine) produces exactly the engine's plnmf_synth_csr stream."""
+    rp, ci, val = O.synth_csr(rows, cols, density, seed)
+    m = P.synth_csr(rows, cols, density, seed)
+    assert (rp == m.row_ptr).all() and (ci == m.col_idx).all() and bits_equal(val, m.values)
