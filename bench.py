@@ -14,7 +14,8 @@ ranks.  One JSON line is printed by rank 0.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 libplnmf compiled from the unmodified sources) on this host's cores, same
-workload and metric.
+workload and metric; its input comes from oracle/synth.c, so that arm never
+loads the engine library.
 """
 from __future__ import annotations
 
@@ -94,6 +95,30 @@ def make_input():
     return P.synth_csr(V, D, DENSITY, GEN_SEED)
 
 
+class _RefCsr:
+    """The same C2 matrix for the reference arm, built by oracle/synth.c (the
+    engine's generator stream restated on the reference side) so that the
+    reference arm never loads the engine library."""
+
+    def __init__(self):
+        from oracle.oracle import synth_csr
+        self.rows, self.cols = V, D
+        self.row_ptr, self.col_idx, self.values = synth_csr(V, D, DENSITY, GEN_SEED)
+
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -122,30 +147,44 @@ def barrier(dist):
 
 
 # ----------------------------------------------------------------------------- reference arm
-def time_reference_cpu(m, steps, warmup, tiled=True, iters_per_step=1):
-    """The reference's iterate() (oracle/_ref) on this host's cores; s/iter with
-    the reference's convention (total - error_eval) / iters (acceptance.cpp:251)."""
+def time_reference_cpu(m, steps, warmup, tiled=True):
+    """The reference's own iterate() (oracle/_ref: libplnmf compiled from the
+    unmodified sources) on this host's cores, as ONE call of
+    max_iters = 1 + warmup + steps with error_every = 1: iteration 1 (which also
+    builds the cached transpose, hals.cpp:26) and `warmup` more are discarded;
+    each timed iteration is its wall-clock delta minus its error evaluation
+    (the reference's convention, (total - error_eval) / iters,
+    acceptance.cpp:251, per iteration), so setup never counts."""
     from oracle.oracle import RefInput, ref, ref_init_factors, ref_iterate
     a = RefInput(m.rows, m.cols, m.row_ptr, m.col_idx, m.values)
     w, ht = ref_init_factors(m.rows, m.cols, K, seed=0)
     cores = ref().ref_max_threads()
-    per = []
-    for i in range(warmup + steps):
-        # continue the trajectory step by step; error evaluated once per call
-        w, ht, tr = ref_iterate(a, w, ht, K, max_iters=iters_per_step, rel_tol=0.0, error_every=iters_per_step,
-                                tile=TILE if tiled else 0, tiled=tiled)
-        if i >= warmup:
-            per.append((tr["total_seconds"] - tr["totals"][8]) / iters_per_step)
+    n = 1 + warmup + steps
+    _, _, tr = ref_iterate(a, w, ht, K, max_iters=n, rel_tol=0.0, error_every=1,
+                           tile=TILE if tiled else 0, tiled=tiled)
+    rec = tr["records"]  # iteration, rel_error, elapsed_s (cumulative), 9 phase buckets (error_eval last)
+    el = rec[:, 2]
+    per = [(el[i] - el[i - 1]) - rec[i, 11] for i in range(1 + warmup, n)]
     return per, cores
 
 
+def reference_sample(steps, warmup, tiled):
+    alg = f"PL-NMF (T={TILE})" if tiled else "FAST-HALS (update_w_reference: serial W update)"
+    return (f"{steps} {alg} iterations of C2 timed inside one reference iterate(max_iters={1 + warmup + steps}, "
+            f"error_every=1) call after {1 + warmup} discarded (setup + warm-up); per iteration = wall delta "
+            f"- error_eval (acceptance.cpp:251 convention); oracle/_ref = the reference compiled from its "
+            f"unmodified sources, OpenMP on all host cores ({cpu_model()})")
+
+
 def reference_arm(args):
-    rank, world, local, dist = dist_setup(args.gpus)
-    if rank != 0:
+    # CPU-only: under torchrun rank 0 alone runs it, the other ranks exit 0 without work
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    m = make_input()
     try:
+        m = _RefCsr()
         per, cores = time_reference_cpu(m, args.steps, args.warmup, tiled=True)
+        fh_steps = 2
+        per_fh, _ = time_reference_cpu(m, fh_steps, 0, tiled=False)
     except ImportError as e:
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return
@@ -157,8 +196,9 @@ def reference_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(m),
         "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} PL-NMF iterations (T={TILE}) of C2 after {args.warmup} warm-up, "
-                                   "reference iterate() compiled from /root/reference sources, OpenMP on all host cores"},
+                         "cpu": cpu_model(), "sample": reference_sample(args.steps, args.warmup, True)},
+        "fast_hals": {"value": 1.0 / float(np.mean(per_fh)), "unit": "iters/s", "cores": cores,
+                      "sample": reference_sample(fh_steps, 0, False)},
         "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -245,8 +285,10 @@ def engine_arm(args):
         try:
             per, cores = time_reference_cpu(m, steps=args.cpu_steps, warmup=1, tiled=True)
             cpu = {"value": 1.0 / float(np.mean(per)), "unit": "iters/s", "cores": cores, "kind": "reference",
-                   "sample": f"{args.cpu_steps} PL-NMF iterations (T={TILE}) of C2 after 1 warm-up, reference "
-                             "iterate() (oracle/_ref, compiled from the reference sources), all host cores"}
+                   "cpu": cpu_model(), "sample": reference_sample(args.cpu_steps, 1, True)}
+            per_fh, _ = time_reference_cpu(m, steps=2, warmup=0, tiled=False)
+            cpu["fast_hals"] = {"value": 1.0 / float(np.mean(per_fh)), "unit": "iters/s",
+                                "sample": reference_sample(2, 0, False)}
         except ImportError as e:
             cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 

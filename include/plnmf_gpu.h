@@ -163,6 +163,11 @@ plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math);
  * (omp_get_max_threads(), `--threads`, proj/tools/plnmf.cpp:104-106), which
  * fixes its tiled norm partials (tiled.cpp:97-99).  Default 1. */
 plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthreads);
+/* Verification hook: on != 0 makes every tiled update take the streaming
+ * plan (stream.cu) that the planner otherwise picks only for shapes whose
+ * per-SM rows do not fit the persistent kernel (C5), so its parity can be
+ * tested on small inputs.  Results are those of the same T either way. */
+plnmf_status plnmf_gpu_force_streaming(plnmf_gpu_engine* e, int32_t on);
 
 /* FactorPair in/out (proj/include/plnmf/workspace.hpp:32-35). */
 plnmf_status plnmf_gpu_set_factors(plnmf_gpu_engine* e, const double* w_colmajor,

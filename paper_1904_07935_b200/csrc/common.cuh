@@ -9,6 +9,17 @@ namespace plnmf {
 
 constexpr int kWarp = 32;
 
+// Timing/diagnostic knobs (PLNMF_DBG, PLNMF_PROFILE, PLNMF_TRACE_EXCHANGE, ...)
+// exist only in a developer build compiled with -DPLNMF_DEBUG_KNOBS
+// (PLNMF_NVCC_EXTRA=-DPLNMF_DEBUG_KNOBS python -m paper_1904_07935_b200.build);
+// the production library never reads the environment and its kernels carry
+// none of the experiment branches.
+#ifdef PLNMF_DEBUG_KNOBS
+constexpr bool kDebugKnobs = true;
+#else
+constexpr bool kDebugKnobs = false;
+#endif
+
 // Arithmetic policy.  Exact: separate round-to-nearest multiply and add, the
 // reference's Release-build arithmetic (no FMA contraction), so per-element
 // sums in the reference's order are bit-identical.  Fused: one fma per term.

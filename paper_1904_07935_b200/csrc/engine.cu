@@ -37,6 +37,7 @@ struct plnmf_gpu_engine {
     // reference's own summation order for the W norms and the error dots (refmode.cu)
     bool ref_order = false;
     int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
+    bool force_streaming = false;  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
 
     int64_t *rp = nullptr, *trp = nullptr;
     int32_t *ci = nullptr, *tci = nullptr;
@@ -174,7 +175,7 @@ void precompute_h(plnmf_gpu_engine* e) {
         std::swap(e->r, e->r_next);
         e->r_valid = false;
         if (e->s_valid) return;
-        e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+        e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
         e->s_valid = true;
         return;
     }
@@ -191,7 +192,7 @@ void precompute_h(plnmf_gpu_engine* e) {
                                       e->k, e->r, e->nnz_t);
     else
         e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
-    if (need_s) e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+    if (need_s) e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
     if (need_s) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
@@ -209,15 +210,15 @@ void precompute_w(plnmf_gpu_engine* e) {
                                       e->k, e->p, e->nnz);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
-    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch);
+    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
     PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
     PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
 }
 
 void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
     if (e->plan_tile == tile) return;
-    e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device);
-    e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device);
+    e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device, e->force_streaming);
+    e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device, e->force_streaming);
     const int64_t qn = kern::qpanel_doubles(e->k, tile);
     if (qn > e->qpanel_n) {
         e->qpanel = dalloc<double>(e, qn);
@@ -248,7 +249,7 @@ void check_tile(const plnmf_config& cfg, int64_t k) {
 }
 
 long long* prof_buffer(plnmf_gpu_engine* e, int grid) {
-    if (!std::getenv("PLNMF_PROFILE")) return nullptr;
+    if (!plnmf::kDebugKnobs || !std::getenv("PLNMF_PROFILE")) return nullptr;
     if (!e->prof || e->prof_n < 24 * (int64_t)grid) {
         e->prof_n = 24 * (int64_t)grid;
         e->prof = dalloc<long long>(e, e->prof_n);
@@ -388,7 +389,7 @@ ErrorReport direct_error(plnmf_gpu_engine* e) {
 // after the reductions).
 ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
     if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_gram: zero input norm");
-    e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch);
+    e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
     e->s_valid = true;
     if (ahead_r) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
@@ -691,6 +692,14 @@ plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
     });
 }
 
+plnmf_status plnmf_gpu_force_streaming(plnmf_gpu_engine* e, int32_t on) {
+    return guarded([&] {
+        check_engine(e);
+        e->force_streaming = on != 0;
+        e->plan_tile = -1;  // re-plan on the next tiled update
+    });
+}
+
 plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthreads) {
     return guarded([&] {
         check_engine(e);
@@ -808,8 +817,9 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which, con
         if (!in) throw std::invalid_argument("plnmf_gpu_set_product: null input");
         int64_t rows, cols;
         double* dst = product_ptr(e, which, rows, cols);
-        if (cols == 1) {
-            PLNMF_CUDA_CHECK(cudaMemcpy(dst, in, sizeof(double) * rows, cudaMemcpyHostToDevice));
+        if (cols == 1) {  // on the engine stream: a pending normalisation must not overwrite it
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(dst, in, sizeof(double) * rows, cudaMemcpyHostToDevice, e->s));
+            PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         } else {
             PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->staging, in, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, e->s));
             e->launches += kern::colmajor_to_rowmajor(e->s, rows, cols, e->staging, dst);
@@ -1038,8 +1048,8 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
                     if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
                     else e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
                     break;
-                case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch); break;
-                case 5: e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch); break;
+                case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms); break;
+                case 5: e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms); break;
                 case 6: precompute_w(e); break;  // Q = gram(Ht) || P = A Ht on two streams
                 case 8:  // S = gram(W) || R = A^T W on two streams
                     e->s_valid = false;
@@ -1092,20 +1102,32 @@ plnmf_status plnmf_gpu_best_integer_tile(plnmf_gpu_engine* e, const plnmf_config
         }
         for (int32_t t : cand)
             if (t < 1 || t > e->k) throw std::invalid_argument("best_integer_tile: tile size must be in [1, K]");
-        double *w0 = nullptr, *h0 = nullptr;
+        // Snapshot of everything a trial update changes — factors, the workspace
+        // products P, Q, R, S, the column norms — restored afterwards together
+        // with the MAC counter, so the call leaves the engine as it found it.
         const size_t wb = sizeof(double) * (size_t)(e->v * e->k), hb = sizeof(double) * (size_t)(e->d * e->k);
-        PLNMF_CUDA_CHECK(cudaMalloc(&w0, wb));
-        PLNMF_CUDA_CHECK(cudaMalloc(&h0, hb));
-        auto restore = [&] {
-            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->w, w0, wb, cudaMemcpyDeviceToDevice, e->s));
-            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->ht, h0, hb, cudaMemcpyDeviceToDevice, e->s));
+        const size_t kb = sizeof(double) * (size_t)(e->k * e->k), nb = sizeof(double) * (size_t)e->k;
+        struct Snap { double** live; size_t bytes; double* copy; };
+        Snap snaps[] = {{&e->w, wb, nullptr}, {&e->ht, hb, nullptr}, {&e->p, wb, nullptr}, {&e->r, hb, nullptr},
+                        {&e->q, kb, nullptr}, {&e->sm, kb, nullptr}, {&e->norms, nb, nullptr}};
+        const uint64_t macs0 = e->update_macs;
+        auto free_snaps = [&] {
+            for (Snap& sn : snaps) if (sn.copy) cudaFree(sn.copy);
+        };
+        auto restore = [&](bool products) {
+            for (Snap& sn : snaps) {
+                if (!products && sn.live != &e->w && sn.live != &e->ht) continue;
+                PLNMF_CUDA_CHECK(cudaMemcpyAsync(*sn.live, sn.copy, sn.bytes, cudaMemcpyDeviceToDevice, e->s));
+            }
             e->s_valid = false;
             e->r_valid = false;
         };
         try {
             PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
-            PLNMF_CUDA_CHECK(cudaMemcpyAsync(w0, e->w, wb, cudaMemcpyDeviceToDevice, e->s));
-            PLNMF_CUDA_CHECK(cudaMemcpyAsync(h0, e->ht, hb, cudaMemcpyDeviceToDevice, e->s));
+            for (Snap& sn : snaps) {
+                PLNMF_CUDA_CHECK(cudaMalloc(&sn.copy, sn.bytes));
+                PLNMF_CUDA_CHECK(cudaMemcpyAsync(sn.copy, *sn.live, sn.bytes, cudaMemcpyDeviceToDevice, e->s));
+            }
             cudaEvent_t a0 = event_at(e, 0), a1 = event_at(e, 1), b0 = event_at(e, 2), b1 = event_at(e, 3);
             double best_ms = 0.0;
             for (size_t i = 0; i < cand.size(); ++i) {
@@ -1113,7 +1135,7 @@ plnmf_status plnmf_gpu_best_integer_tile(plnmf_gpu_engine* e, const plnmf_config
                 c.tile_size = cand[i];
                 double ms = 0.0;
                 for (int rep = 0; rep < 2; ++rep) {  // warm-up (plans, coefficient panels), then timed
-                    restore();
+                    restore(false);
                     precompute_h(e);
                     PLNMF_CUDA_CHECK(cudaEventRecord(a0, e->s));
                     update_h(e, c, PLNMF_ALGORITHM_TILED);
@@ -1131,15 +1153,14 @@ plnmf_status plnmf_gpu_best_integer_tile(plnmf_gpu_engine* e, const plnmf_config
                     *best = cand[i];
                 }
             }
-            restore();
+            restore(true);
             PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+            e->update_macs = macs0;
         } catch (...) {
-            cudaFree(w0);
-            cudaFree(h0);
+            free_snaps();
             throw;
         }
-        PLNMF_CUDA_CHECK(cudaFree(w0));
-        PLNMF_CUDA_CHECK(cudaFree(h0));
+        free_snaps();
     });
 }
 

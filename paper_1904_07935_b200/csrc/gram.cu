@@ -311,7 +311,7 @@ int64_t gram_scratch_doubles(int64_t n, int64_t k) {
 }
 
 int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double* g,
-         double* scratch) {
+         double* scratch, int sms) {
     if (k <= 0) return 0;
     const int64_t nblk = (n + kGramBlock - 1) / kGramBlock;
     if (nblk == 0) {
@@ -321,11 +321,8 @@ int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double
     const int ntile = (int)((k + kGramTile - 1) / kGramTile);
     const dim3 grid((unsigned)(ntile * (ntile + 1) / 2), (unsigned)(2 * nblk));
     // fewer than ~4 CTAs per SM of 4x4 threads: use 4x2 threads (twice the warps)
-    int dev = 0, sms = 148;
-    PLNMF_CUDA_CHECK(cudaGetDevice(&dev));
-    PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const bool narrow = (int64_t)grid.x * grid.y < 8LL * sms;
-    const int variant = std::getenv("PLNMF_GRAM_TILE") ? std::atoi(std::getenv("PLNMF_GRAM_TILE")) : (narrow ? 42 : 44);
+    const bool narrow = (int64_t)grid.x * grid.y < 8LL * sms;  // sms: the engine's device (cached by the caller)
+    const int variant = narrow ? 42 : 44;
     if (m == Math::exact) {
         if (variant == 22) gram_block_kernel<MathExact, 2, 2><<<grid, 256, 0, s>>>(n, (int)k, mat, scratch, ntile);
         else if (variant == 42) gram_block_kernel<MathExact, 2, 4><<<grid, 128, 0, s>>>(n, (int)k, mat, scratch, ntile);

@@ -38,8 +38,9 @@ int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int3
 // order (2048-row blocks, even/odd lanes, proj/src/linalg.cpp:168-204).
 // scratch: gram_scratch_doubles(n, k) doubles.
 int64_t gram_scratch_doubles(int64_t n, int64_t k);
+// sms: the device's SM count (selects the CTA shape; the caller caches it).
 int gram(cudaStream_t s, Math m, int64_t n, int64_t k, const double* mat, double* g,
-         double* scratch);
+         double* scratch, int sms = 148);
 
 // Dense products for a dense input A (row-major v x d on the device).
 // p := A * ht    (proj/src/hals.cpp:43 -> accumulate_nn, linalg.cpp:45-59)
@@ -69,7 +70,9 @@ int64_t qpanel_doubles(int64_t k, int64_t tile);
 // (:52-65), and per tile phase 2 (:67-156) + phase 3 (:158-174).  w_update =>
 // init scales by the diagonal and every column is L2-normalised with a
 // grid-wide exchange (cooperative persistent launch, one CTA per SM).
-PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
+// force_streaming: take the streaming fallback whatever the shape (verification).
+PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device,
+                             bool force_streaming = false);
 // Streaming fallback (stream.cu): phase A + one persistent streaming launch.
 PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,

@@ -178,13 +178,19 @@ namespace kern {
 int64_t exchange_partials_doubles(int64_t k, int g) { return xch_partials(k, g); }
 int64_t exchange_counters(int64_t k) { return xch_counters(k); }
 
-PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device) {
+namespace {
+// developer-build knobs only (common.cuh: kDebugKnobs); always false in production
+bool knob(const char* name) { return kDebugKnobs && std::getenv(name) != nullptr; }
+int knob_int(const char* name) { return knob(name) ? std::atoi(std::getenv(name)) : 0; }
+}  // namespace
+
+PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device, bool force_streaming) {
     PhaseBPlan plan;
     int max_smem = 0;
     PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     const int sms = sm_count(device);
     int64_t rpc = n > 0 ? (n + sms - 1) / sms : 1;  // one SM's share of rows
-    if (std::getenv("PLNMF_FORCE_STREAMING")) return plan_stream_update(n, k, tile, normalize, device);
+    if (force_streaming) return plan_stream_update(n, k, tile, normalize, device);
     // shared-memory variants, most staged first
     const bool variants[3][2] = {{true, true}, {false, true}, {false, false}};
     // the staged look-ahead GEMM wants >= 8-wide operand chunks; an unstaged
@@ -219,7 +225,7 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
         // the staged GEMM runs items (row x 16 columns) round-robin over the look-ahead threads
         const int nupd = pl_nupd(rpc, normalize);
         const int64_t items = rpc * ((std::min<int64_t>(tile, k) + 15) / 16);
-        if (!std::getenv("PLNMF_NO_STAGED_GEMM") && plan.sqn_smem && items <= 4 * (int64_t)nupd)
+        if (!knob("PLNMF_NO_STAGED_GEMM") && plan.sqn_smem && items <= 4 * (int64_t)nupd)
             for (int st : {3, 2})
                 if (pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, kPrivKC, st, normalize) <= (size_t)max_smem) {
                     plan.kc = kPrivKC;
@@ -229,7 +235,7 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
                 }
     }
     plan.smem = pl_smem(rpc, k, tile, plan.stage_ops, plan.sqn_smem, plan.kc, plan.kst, normalize);
-    if (!normalize && tile <= 16 && !std::getenv("PLNMF_NO_RESIDENT")) {
+    if (!normalize && tile <= 16 && !knob("PLNMF_NO_RESIDENT")) {
         // H: keep the CTA's rows resident in shared memory when they fit (no
         // staging, no oldB), up to 4 rows per look-ahead thread of a column
         const int64_t tq = (tile + 7) & ~int64_t(7);
@@ -262,17 +268,17 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
         return stream_update(s, m, plan, n, k, tile, eps, w_update, old_m, out, coeff, add, norms, partials,
                              counters);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
-               norms, partials, counters, totals, prof, std::getenv("PLNMF_NO_OVERLAP") ? 0 : std::getenv("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1, nullptr,
-               qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
-               std::getenv("PLNMF_DBG") ? std::atoi(std::getenv("PLNMF_DBG")) : 0, plan.resident, (int)k + 2};
+               norms, partials, counters, totals, prof, knob("PLNMF_NO_OVERLAP") ? 0 : knob("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1,
+               nullptr, qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
+               knob_int("PLNMF_DBG"), plan.resident, (int)k + 2};
     {
         const int tq = (int)((tile + 7) & ~int64_t(7));
         qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(
             (int)k, (int)tile, tq, coeff, qpanel);
         PLNMF_CUDA_CHECK(cudaGetLastError());
     }
-    static unsigned long long* trace_buf = nullptr;
-    if (w_update && std::getenv("PLNMF_TRACE_EXCHANGE")) {
+    static unsigned long long* trace_buf = nullptr;  // developer builds only (one process, one device)
+    if (w_update && knob("PLNMF_TRACE_EXCHANGE")) {
         if (!trace_buf) PLNMF_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(unsigned long long) * kTraceSlots * 1024 * 512));
         a.trace = trace_buf;
         PLNMF_CUDA_CHECK(cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * kTraceSlots * 1024 * 512, s));
@@ -286,7 +292,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
         else launch_pl<MathFused, false>(s, plan, a);
     }
     PLNMF_CUDA_CHECK(cudaGetLastError());
-    if (a.trace) {
+    if (kDebugKnobs && a.trace) {
         const int g = plan.grid;
         std::vector<unsigned long long> h((size_t)kTraceSlots * k * g);
         PLNMF_CUDA_CHECK(cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
@@ -338,7 +344,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                          "->phase-3 done %.0f, ->coeff block + sync %.0f, ->first value %.0f\n",
                          bs[0] / nb, bs[1] / nb, bs[2] / nb, bs[3] / nb, bs[4] / nb);
     }
-    return 1;
+    return 2;  // qpanel_kernel + pl_update_kernel
 }
 
 int reference_update_h(cudaStream_t s, Math m, int64_t d, int64_t k, double eps, double* ht,

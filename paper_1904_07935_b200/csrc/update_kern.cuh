@@ -113,6 +113,10 @@ __device__ __forceinline__ void row_panel(double (&acc)[C], const double* __rest
 // shared-memory path for tiles wider than 32.
 template <class M, bool NORMALIZE, int TMAX, bool STAGE, bool SQN>
 __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
+    // developer-build instrumentation (common.cuh: kDebugKnobs); compiled out in production
+    unsigned long long* const ptrace = kDebugKnobs ? p.trace : nullptr;
+    long long* const pprof = kDebugKnobs ? p.prof : nullptr;
+    const int overlap = kDebugKnobs ? p.overlap : 1;
     extern __shared__ double smem[];
     const int T = p.tile, k = p.k, ldt = T + 1;
     const int TQ = (T + 7) & ~7;  // sqn leading dimension: whole 8-column panels, 16-byte rows
@@ -157,9 +161,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // add section durations straight to global (profiling runs only); no
     // per-section registers in production.
     long long* const prof_row =
-        p.prof ? ((tid == 0) ? p.prof + blockIdx.x * 24
-                  : (tid == nupd) ? p.prof + blockIdx.x * 24 + 8
-                  : (is_xwarp && ctid == nrowt) ? p.prof + blockIdx.x * 24 + 16 : nullptr)
+        pprof ? ((tid == 0) ? pprof + blockIdx.x * 24
+                  : (tid == nupd) ? pprof + blockIdx.x * 24 + 8
+                  : (is_xwarp && ctid == nrowt) ? pprof + blockIdx.x * 24 + 16 : nullptr)
                : nullptr;
     long long t0 = prof_row ? clock64() : 0;
     auto mark = [&](int sec) {
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     // last tile may be narrower) is published to global by the look-ahead warps at the start
     // of the next tile, before build_next reuses its buffer, instead of by the chain at the
     // tile boundary
-    const bool la_pub = NORMALIZE && kExactM<M> && TMAX > 0 && p.overlap == 1 && !p.resident;
+    const bool la_pub = NORMALIZE && kExactM<M> && TMAX > 0 && overlap == 1 && !p.resident;
     auto publish_prev = [&](const double* P, int pb) {
         if (T == 16) {
             for (int idx = utid; idx < nrows * 16; idx += nupd)
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         double* A = acc[cur];
         // PLNMF_TRACE_EXCHANGE: tile-boundary stamps go to the tile's last column
         unsigned long long* const btr =
-            p.trace ? p.trace + ((int64_t)(e - 1) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
+            ptrace ? ptrace + ((int64_t)(e - 1) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
         if (is_chain && TMAX > 0 && NORMALIZE && kExactM<M>) {
             // ---- W phase 2, latency-ordered (Math::exact).  Everything that does
             // not depend on the column's norm is computed while the exchange is
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                     val = clamp_floor(p.eps, dsub(dadd(arow[0], add0), s));
                 }
             }
-            if (p.trace && b > 0 && ctid == 0) p.trace[((int64_t)(b - 1) * gridDim.x + blockIdx.x) * kTraceSlots + 13] = clock64();
+            if (ptrace && b > 0 && ctid == 0) ptrace[((int64_t)(b - 1) * gridDim.x + blockIdx.x) * kTraceSlots + 13] = clock64();
             // the additive term is read from global one column ahead of its use
             // (an HBM/L2 load: ~1K cycles that the prefix would otherwise stall on)
             double add_nx = (own && w > 1) ? addr[1] : 0.0;
@@ -389,10 +393,10 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             for (int tt = 0; tt < w; ++tt) {
                 {
                     unsigned long long* const trc =
-                        p.trace ? p.trace + ((int64_t)(b + tt) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
+                        ptrace ? ptrace + ((int64_t)(b + tt) * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
                     const bool more = tt + 1 < w;
                     if (!is_xwarp) {
-                        const double ss = (p.dbg & 8) ? val : warp_sum_lane0(dmul(val, val));
+                        const double ss = (kDebugKnobs && (p.dbg & 8)) ? val : warp_sum_lane0(dmul(val, val));
                         if (lane_id() == 0) red[ctid >> 5] = ss;
                     }
                     mark(kProfDot);
@@ -408,9 +412,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         const double blk = tree8(v);
                         mark(kProfChain);
                         if (trc && lane_id() == 0) trc[7] = clock64();
-                        const double norm = (p.dbg & 32) ? __dsqrt_rn(blk)
+                        const double norm = (kDebugKnobs && (p.dbg & 32)) ? __dsqrt_rn(blk)
                                                          : grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters,
-                                                                         p.trace);
+                                                                         ptrace);
                         if (lane_id() == 0) {
                             red[40] = norm;
                             // the rows divide as a * RN(1/norm) + one fma correction: bit-identical to
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         mark(kProfGrid);
                     } else if (own && !more && has_next) {
                         add_carry = addr[w];  // next tile's first column
-                    } else if (own && more && !(p.dbg & 1)) {
+                    } else if (own && more && !(kDebugKnobs && (p.dbg & 1))) {
                         // next column's norm-independent parts, overlapping the exchange
 #pragma unroll
                         for (int j = 0; j < TM; ++j)
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         arow[tt] = nv;
                         if (more) {
                             double s2 = dadd(pre, dmul(nv, c1));
-                            if (!(p.dbg & 2))
+                            if (!(kDebugKnobs && (p.dbg & 2)))
 #pragma unroll
                                 for (int j = 0; j < TM; ++j)
                                     if (j > tt && j < w) s2 = dadd(s2, prod[j]);
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                             blk = __shfl_sync(0xffffffffu, blk, 0);
                             mark(kProfChain);
                             const double norm =
-                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, p.trace);
+                                grid_exchange(blk, b + tt, gridDim.x, p.partials, p.counters, ptrace);
                             if (lane_id() == 0) {
                                 red[40] = norm;
                                 if (blockIdx.x == 0) p.norms[b + tt] = norm;
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                         }
                         blk = __shfl_sync(0xffffffffu, blk, 0);
                         mark(kProfChain);
-                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters, p.trace);
+                        const double norm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters, ptrace);
                         if (lane_id() == 0) {
                             red[40] = norm;
                             if (blockIdx.x == 0) p.norms[t] = norm;
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 if (p.resident) resid[r * p.ldr + b + j] = A[r * ldt + j];
             }
             mark(kProfChain);
-        } else if (has_next && p.overlap) {
+        } else if (has_next && overlap) {
             // ---- look-ahead: next tile's accumulators, minus this tile's phase-3 term
             if (la_pub && b > 0) publish_prev(acc[cur ^ 1], b - T);  // before build_next reuses it
             load_sqn(bn, en, utid, nupd);
@@ -624,8 +628,8 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
 #ifndef PLNMF_CHAIN_ONLY  // timing experiment: the chain with the look-ahead compiled out
             {
                 // PLNMF_DBG >> 8: look-ahead width in warps (timing experiments only; 0 = all)
-                const int nla = (p.dbg >> 8) ? min((p.dbg >> 8) * kWarp, nupd) : nupd;
-                if (p.overlap != 2 && utid < nla) build_next(acc[cur ^ 1], bn, en, b, 0, nla, utid);  // 2: timing probe only
+                const int nla = (kDebugKnobs && (p.dbg >> 8)) ? min((p.dbg >> 8) * kWarp, nupd) : nupd;
+                if ((!kDebugKnobs || overlap != 2) && utid < nla) build_next(acc[cur ^ 1], bn, en, b, 0, nla, utid);  // 2: timing probe only
             }
 #endif
             mark(kProfUpd);
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         if (btr && tid == nupd) btr[10] = clock64();
         mark(kProfWait);
 #ifndef PLNMF_CHAIN_ONLY
-        if (has_next && !p.overlap) {
+        if (has_next && !overlap) {
             load_sqn(bn, en, tid, kLThreads);
             stage_tile(cur ^ 1, bn, en, tid, kLThreads);
             cp_async_wait<0>();

@@ -314,6 +314,10 @@ class Engine:
     def set_math(self, math: Math) -> None:
         _check(L.lib().plnmf_gpu_set_math(self._h, int(math)))
 
+    def force_streaming(self, on: bool = True) -> None:
+        """Verification hook: tiled updates take the streaming plan (stream.cu)."""
+        _check(L.lib().plnmf_gpu_force_streaming(self._h, int(bool(on))))
+
     def set_reference_threads(self, n: int) -> None:
         """Math.reference_order: the reference's OpenMP team size (its tiled
         norm partials depend on it, proj/src/tiled.cpp:97-99)."""

@@ -119,8 +119,8 @@ def test_streaming_fallback_updates(gpu, k, tile, monkeypatch):
     streaming launch; the planner's choice when one SM's rows do not fit the
     persistent kernel, e.g. C5), forced on a small instance: H bitwise, W to
     1e-12 (norm reduction order only)."""
-    monkeypatch.setenv("PLNMF_FORCE_STREAMING", "1")
     m, eng, f = make(2500, 1300, 0.01, k)
+    eng.force_streaming(True)
     eng.precompute_h_products()
     r, s = eng.get_product("r"), eng.get_product("s")
     cfg = P.SolverConfig(rank=k, tile_size=tile)
