@@ -241,11 +241,14 @@ def engine_arm(args):
     step_ms = []
     barrier(dist)
     torch.cuda.synchronize()
+    phase_tot = {}
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             step_ms.append(eng.run_iterations(cfg, alg, 1))
+            for k2, v2 in eng.phase_ms().items():  # CUDA events on the engine stream, inside the timed steps
+                phase_tot[k2] = phase_tot.get(k2, 0.0) + v2
     torch.cuda.synchronize()
     barrier(dist)
     launches = eng.stats()["kernel_launches"] - launches0
@@ -270,13 +273,21 @@ def engine_arm(args):
     # dominant kernel by share of the step (two SpMMs per step)
     shares = {"spmm": kt["spmm_A_Ht"] + kt["spmm_At_W"], "update_w_tiled": kt["update_w_tiled"],
               "update_h_tiled": kt["update_h_tiled"], "gram": 2 * kt["gram_W"]}
-    # W update algorithmic bytes: read W, P, write+read the accumulator, write W_new
-    b_w = 8 * V * K * 4 + 8 * K * K
+    # W update (the dominant kernel) compulsory bytes: read W and P, write W_new (V x K each), read Q
+    b_w = 3 * 8 * V * K + 8 * K * K
+    w_ms = phase_tot["update_w"] / args.steps  # per launch, measured inside the timed steps
+    rl_w = b_w / (w_ms * 1e-3) / 1e9
+    roofline = {"kernel": "pl_update_kernel (W update, tiled; the step's dominant kernel)", "bound": "hbm",
+                "achieved": rl_w, "peak": hbm, "unit": "GB/s", "frac": rl_w / hbm,
+                "traffic": ncu_traffic("wupdate"), "algorithmic_bytes": b_w, "launch_ms": w_ms,
+                "share_of_step": w_ms / (total_ms / args.steps),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback",
+                # what actually bounds it: K = 240 dependent grid-wide norm reductions (tiled.cpp:92-148)
+                "latency": {"us_per_column": w_ms * 1e3 / K, "isolated_chain_plus_exchange_us": 1.73,
+                            "frac_of_floor": 1.73 / (w_ms * 1e3 / K),
+                            "source": "tools/chain_bench.cu, tools/exchange_bench2.cu (profiles/r1_microbench.txt)"}}
     rl_spmm = b_p / (kt["spmm_A_Ht"] * 1e-3) / 1e9
-    roofline = {"kernel": "spmm_csr A*Ht (K1)", "bound": "hbm", "achieved": rl_spmm, "peak": hbm, "unit": "GB/s",
-                "frac": rl_spmm / hbm, "traffic": ncu_traffic("spmm"),
-                "algorithmic_bytes": b_p, "launch_ms": kt["spmm_A_Ht"],
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback"}
+    l2 = l2_peak()
     # e2e through the reference-facing C-ABI call with host factors
     e2e = e2e_arm(P, a, eng, cfg, alg, args, torch)
 
@@ -300,17 +311,18 @@ def engine_arm(args):
             "math": args.math, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "warm_l2_ms_per_iter": warm_ms,
             "kernels_ms": kt, "kernel_share_of_step": {k2: v2 / step for k2, v2 in shares.items()},
+            "phase_ms_per_step": {k2: v2 / args.steps for k2, v2 in phase_tot.items()},
+            # the SpMMs (BASELINE metric's second half) against HBM and against the
+            # measured L2 gather ceiling that actually bounds them (Finding 3)
             "spmm_roofline": {"A_Ht_GBps": rl_spmm, "At_W_GBps": b_r / (kt["spmm_At_W"] * 1e-3) / 1e9,
-                              "bytes_A_Ht": b_p, "bytes_At_W": b_r,
-                              "l2_gather_bytes": 8 * nnz * K},
-            "update_w_bytes": b_w,
-            # the step's dominant kernel is neither HBM- nor tensor-bound: it is the W
-            # update's chain of K grid-wide norm exchanges
-            "dominant_kernel": {"kernel": "pl_update_kernel (W, tiled)", "share_of_step": kt["update_w_tiled"] / step,
-                                "bound": "latency (K dependent grid-wide reductions)",
-                                "us_per_column": kt["update_w_tiled"] * 1e3 / K,
-                                "isolated_exchange_us": 1.28, "isolated_chain_plus_exchange_us": 1.73,
-                                "source": "tools/exchange_bench2.cu, tools/chain_bench.cu (profiles/)"},
+                              "hbm_frac_A_Ht": rl_spmm / hbm, "bytes_A_Ht": b_p, "bytes_At_W": b_r,
+                              "l2_gather_bytes": 8 * nnz * K,
+                              "l2_gather_GBps": 8 * nnz * K / (kt["spmm_A_Ht"] * 1e-3) / 1e9,
+                              "l2_gather_peak_GBps": l2.get("gather_l2_gbs_16B"),
+                              "l2_frac": (8 * nnz * K / (kt["spmm_A_Ht"] * 1e-3) / 1e9 / l2["gather_l2_gbs_16B"])
+                              if l2.get("gather_l2_gbs_16B") else None,
+                              "l2_peak_source": "profiles/l2_peak.json (tools/l2bw_bench.cu on a B200)",
+                              "traffic": ncu_traffic("spmm")},
             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
         }
         print(json.dumps(line), flush=True)
@@ -359,6 +371,13 @@ def e2e_arm(P, a, eng, cfg, alg, args, torch):
             "what": f"plnmf_gpu_iterate_host(max_iters={E2E_ITERS}, error_every=1, rel_tol=0) on pinned host W,Ht "
                     "(col-major f64): upload, 100 iterations with the reference's per-iteration error evaluation "
                     "and stop-rule check, download; host wall clock"}
+
+
+def l2_peak():
+    try:
+        return json.loads((ROOT / "profiles" / "l2_peak.json").read_text())
+    except Exception:
+        return {}
 
 
 def ncu_traffic(kernel):

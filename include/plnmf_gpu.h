@@ -38,7 +38,8 @@ typedef enum plnmf_status {
     PLNMF_RUNTIME = 2,
     PLNMF_DOMAIN = 3,
     PLNMF_CUDA = 4,
-    PLNMF_NCCL = 5
+    PLNMF_NCCL = 5,
+    PLNMF_PARSE = 6  /* plnmf::ParseError (a std::runtime_error), "source:line: what" */
 } plnmf_status;
 
 /* proj/include/plnmf/config.hpp:9 — Algorithm{reference, tiled}
@@ -120,6 +121,10 @@ typedef struct plnmf_gpu_stats {
     int32_t persistent_ctas;   /* CTAs of the grid-synchronised W update */
     int32_t sm_count;
     int64_t device_bytes;      /* device memory held by the engine */
+    /* plan of the last tiled W / H update: 0 persistent look-ahead with the tile's
+     * operands and the coefficient panel staged in shared memory, 1 panel staged
+     * only, 2 neither staged, 3 streaming (stream.cu); -1 none yet */
+    int32_t w_plan, h_plan;
 } plnmf_gpu_stats;
 
 /* ---- host-side helpers (no GPU needed) --------------------------------------- */
@@ -141,6 +146,22 @@ plnmf_status plnmf_init_factors(int64_t v, int64_t d, const plnmf_config* cfg, d
 plnmf_status plnmf_synth_csr(int64_t rows, int64_t cols, double density, uint64_t seed,
                              int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz);
 
+/* ---- Matrix Market input (proj/src/matrix_market.cpp) ---------------
+ * plnmf_mm_read parses like read_matrix_market (same banner rules — coordinate
+ * real/pattern general or array real general —, comment/blank-line skipping,
+ * checks, messages and line numbers; failures return PLNMF_PARSE with
+ * "path:line: what").  The parsed entries stay on the host in file order;
+ * plnmf_gpu_create_mm assembles the CSR on the device (rows bucketed, each row
+ * sorted by column keeping file order, duplicates summed in file order,
+ * matrix_market.cpp:147-172) or uploads the dense array. */
+typedef struct plnmf_mm plnmf_mm;
+plnmf_status plnmf_mm_read(const char* path, plnmf_mm** out);
+/* The same parser on an in-memory text (the istream overload, matrix_market.hpp:29). */
+plnmf_status plnmf_mm_read_string(const char* text, const char* source_name, plnmf_mm** out);
+/* entries = declared coordinate entries (before duplicate summation) or rows*cols. */
+plnmf_status plnmf_mm_info(const plnmf_mm* m, int64_t* rows, int64_t* cols, int64_t* entries, int32_t* sparse);
+plnmf_status plnmf_mm_free(plnmf_mm* m);
+
 /* ---- engine -------------------------------------------------------------------- */
 int32_t plnmf_gpu_device_count(void);
 
@@ -154,6 +175,21 @@ plnmf_status plnmf_gpu_create_csr(int32_t device, int64_t rows, int64_t cols, in
 plnmf_status plnmf_gpu_create_dense(int32_t device, int64_t rows, int64_t cols,
                                     const double* a_colmajor, int64_t rank,
                                     plnmf_gpu_engine** out);
+/* An engine on a parsed Matrix Market file (InputMatrix(read_matrix_market(path))). */
+plnmf_status plnmf_gpu_create_mm(int32_t device, const plnmf_mm* m, int64_t rank, plnmf_gpu_engine** out);
+/* An engine on the SURVEY.md 8(d) synthetic CSR generated ON THE DEVICE (the
+ * stream of plnmf_synth_csr; the large config's ~1e9 nonzeros never touch the
+ * host).  ||A||^2 is still summed serially in the reference's order
+ * (input_matrix.cpp:15-20) from the device values. */
+plnmf_status plnmf_gpu_create_synthetic(int32_t device, int64_t rows, int64_t cols, double density, uint64_t seed,
+                                        int64_t rank, plnmf_gpu_engine** out);
+/* The device CSR of a sparse engine's A (row_ptr rows+1, col_idx/values nnz). */
+plnmf_status plnmf_gpu_get_csr(plnmf_gpu_engine* e, int64_t* row_ptr, int64_t* col_idx, double* values);
+/* Rows of a sparse engine's A (transposed = 0) or of its device-built A^T
+ * (transposed = 1): for the n row indices, row_ptr_out (n+1, offsets into the
+ * outputs) and, when col_idx/values are non-NULL, the entries. */
+plnmf_status plnmf_gpu_get_csr_rows(plnmf_gpu_engine* e, int32_t transposed, const int64_t* rows, int64_t n,
+                                    int64_t* row_ptr_out, int64_t* col_idx, double* values);
 plnmf_status plnmf_gpu_destroy(plnmf_gpu_engine* e);
 /* InputMatrix::norm_sq / nnz / rows / cols (input_matrix.hpp:17-28). */
 plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int64_t* cols,
@@ -237,6 +273,11 @@ plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int64_t v, in
 /* Device pointer and shape of an engine buffer (row-major fp64), for the caller's collectives. */
 plnmf_status plnmf_gpu_buffer(plnmf_gpu_engine* e, plnmf_buffer which, void** dev_ptr, int64_t* rows,
                               int64_t* cols);
+/* Rows of an engine buffer (PLNMF_BUF_W, _HT, _P, _R; local rows on a shard):
+ * out = n x K row-major, out[i*K + j] = buffer(rows[i], j).  For sampled parity
+ * checks on inputs too large to download whole (C5). */
+plnmf_status plnmf_gpu_get_rows(plnmf_gpu_engine* e, plnmf_buffer which, const int64_t* rows, int64_t n,
+                                double* out);
 /* W_full[v_lo:v_hi] := W local; Ht_full[d_lo:d_hi] := Ht local (before the caller's gathers). */
 plnmf_status plnmf_gpu_shard_publish(plnmf_gpu_engine* e);
 /* Column-stepped tiled W update (tiled.cpp:176-193): begin = init + phase 1; per column t of
@@ -255,6 +296,10 @@ plnmf_status plnmf_gpu_local_pw(plnmf_gpu_engine* e, double* out);
  * timed with CUDA events on the engine stream; *device_ms = total. */
 plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* cfg,
                                       plnmf_algorithm algorithm, int64_t n, double* device_ms);
+/* Device time of each step of the last plnmf_gpu_run_iterations call, summed over
+ * its iterations (CUDA events on the engine stream between the steps):
+ * out4 = {precompute_h (R, S), update_h, precompute_w (P, Q), update_w} in ms. */
+plnmf_status plnmf_gpu_phase_ms(const plnmf_gpu_engine* e, double* out4);
 /* Times `reps` launches of one engine kernel family on the current state:
  * 0 = SpMM A*Ht (P), 1 = SpMM A^T*W (R), 2 = gram(W), 3 = W update, 4 = H update.
  * *avg_ms = mean CUDA-event duration per launch (events on the engine stream). */

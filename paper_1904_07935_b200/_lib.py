@@ -37,7 +37,7 @@ class TraceC(C.Structure):
 
 class StatsC(C.Structure):
     _fields_ = [("kernel_launches", u64), ("persistent_ctas", i32), ("sm_count", i32),
-                ("device_bytes", i64)]
+                ("device_bytes", i64), ("w_plan", i32), ("h_plan", i32)]
 
 
 Engine_p = C.c_void_p
@@ -52,6 +52,15 @@ SIGNATURES = {
     "plnmf_plan_tiles": (C.c_int, [i64, i64, P_i64, P_i64, P_i64]),
     "plnmf_init_factors": (C.c_int, [i64, i64, P_cfg, P_f64, P_f64]),
     "plnmf_synth_csr": (C.c_int, [i64, i64, f64, u64, P_i64, P_i64, P_f64, P_i64]),
+    "plnmf_mm_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "plnmf_mm_read_string": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "plnmf_mm_info": (C.c_int, [C.c_void_p, P_i64, P_i64, P_i64, C.POINTER(C.c_int32)]),
+    "plnmf_mm_free": (C.c_int, [C.c_void_p]),
+    "plnmf_gpu_create_mm": (C.c_int, [i32, C.c_void_p, i64, C.POINTER(Engine_p)]),
+    "plnmf_gpu_create_synthetic": (C.c_int, [i32, i64, i64, f64, u64, i64, C.POINTER(Engine_p)]),
+    "plnmf_gpu_get_csr": (C.c_int, [Engine_p, P_i64, P_i64, P_f64]),
+    "plnmf_gpu_get_csr_rows": (C.c_int, [Engine_p, i32, P_i64, i64, P_i64, P_i64, P_f64]),
+    "plnmf_gpu_get_rows": (C.c_int, [Engine_p, C.c_int, P_i64, i64, P_f64]),
     "plnmf_gpu_device_count": (i32, []),
     "plnmf_gpu_create_csr": (C.c_int, [i32, i64, i64, i64, P_i64, P_i64, P_f64, i64, C.POINTER(Engine_p)]),
     "plnmf_gpu_create_dense": (C.c_int, [i32, i64, i64, P_f64, i64, C.POINTER(Engine_p)]),
@@ -84,6 +93,7 @@ SIGNATURES = {
     "plnmf_gpu_w_end": (C.c_int, [Engine_p]),
     "plnmf_gpu_local_pw": (C.c_int, [Engine_p, P_f64]),
     "plnmf_gpu_run_iterations": (C.c_int, [Engine_p, P_cfg, C.c_int, i64, P_f64]),
+    "plnmf_gpu_phase_ms": (C.c_int, [Engine_p, P_f64]),
     "plnmf_gpu_time_kernel": (C.c_int, [Engine_p, P_cfg, i32, i32, P_f64]),
     "plnmf_gpu_best_integer_tile": (C.c_int, [Engine_p, P_cfg, C.POINTER(C.c_int32), i32, C.POINTER(C.c_int32),
                                               P_f64]),

@@ -37,7 +37,8 @@ struct plnmf_gpu_engine {
     // reference's own summation order for the W norms and the error dots (refmode.cu)
     bool ref_order = false;
     int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
-    bool force_streaming = false;  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
+    bool force_streaming = false;
+    double last_phase_ms[4] = {0, 0, 0, 0};  // run_iterations: precompute_h, update_h, precompute_w, update_w  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
 
     int64_t *rp = nullptr, *trp = nullptr;
     int32_t *ci = nullptr, *tci = nullptr;
@@ -580,6 +581,64 @@ void validate_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp, co
     }
 }
 
+template <class T>
+void adopt(plnmf_gpu_engine* e, T* ptr, int64_t n) {
+    e->allocs.push_back(ptr);
+    e->bytes += (int64_t)(sizeof(T) * (size_t)std::max<int64_t>(1, n));
+}
+
+// A sparse engine on a CSR that already lives on the device (device generator,
+// Matrix Market assembly): takes ownership of the arrays, sums ||A||^2 serially
+// in the reference's order (input_matrix.cpp:15-20) from the device values
+// (streamed to the host in chunks; also InputMatrix's finiteness check), builds
+// A^T on the device and the workspace.
+void finish_device_csr(plnmf_gpu_engine* e, int64_t rows, int64_t cols, int64_t nnz, int64_t* rp, int32_t* ci,
+                       double* val) {
+    adopt(e, rp, rows + 1);
+    adopt(e, ci, nnz);
+    adopt(e, val, nnz);
+    if (cols > INT32_MAX || rows > INT32_MAX)
+        throw std::invalid_argument("plnmf_gpu_create: dimensions exceed int32 column indexing");
+    e->v = rows;
+    e->d = cols;
+    e->nnz = nnz;
+    e->nnz_t = nnz;
+    e->sparse = true;
+    e->rp = rp;
+    e->ci = ci;
+    e->val = val;
+    {
+        constexpr int64_t kChunk = 1 << 23;
+        double* host = nullptr;
+        PLNMF_CUDA_CHECK(cudaMallocHost(&host, sizeof(double) * (size_t)std::min<int64_t>(kChunk, std::max<int64_t>(1, nnz))));
+        double n2 = 0.0;
+        bool finite = true;
+        try {
+            for (int64_t b = 0; b < nnz; b += kChunk) {
+                const int64_t m = std::min(kChunk, nnz - b);
+                PLNMF_CUDA_CHECK(cudaMemcpyAsync(host, val + b, sizeof(double) * m, cudaMemcpyDeviceToHost, e->s));
+                PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+                for (int64_t i = 0; i < m; ++i) {
+                    finite = finite && std::isfinite(host[i]) && host[i] >= 0.0;
+                    n2 += host[i] * host[i];
+                }
+            }
+        } catch (...) {
+            cudaFreeHost(host);
+            throw;
+        }
+        PLNMF_CUDA_CHECK(cudaFreeHost(host));
+        if (!finite) throw std::invalid_argument("CsrMatrix: values must be finite and non-negative");
+        e->a2 = n2;
+    }
+    e->trp = dalloc<int64_t>(e, cols + 1);
+    e->tci = dalloc<int32_t>(e, nnz);
+    e->tval = dalloc<double>(e, nnz);
+    e->launches += kern::csr_transpose(e->s, rows, cols, nnz, e->rp, e->ci, e->val, e->trp, e->tci, e->tval);
+    alloc_workspace(e);
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+}
+
 }  // namespace
 
 // =============================================================================== C-ABI
@@ -664,6 +723,128 @@ plnmf_status plnmf_gpu_create_dense(int32_t device, int64_t rows, int64_t cols, 
     });
     if (st != PLNMF_OK) release(e);
     return st;
+}
+
+plnmf_status plnmf_gpu_create_synthetic(int32_t device, int64_t rows, int64_t cols, double density, uint64_t seed,
+                                        int64_t rank, plnmf_gpu_engine** out) {
+    plnmf_gpu_engine* e = nullptr;
+    const plnmf_status st = guarded([&] {
+        if (!out) throw std::invalid_argument("plnmf_gpu_create_synthetic: null output");
+        e = new plnmf_gpu_engine();
+        setup_common(e, device, rank);
+        int64_t* rp = nullptr;
+        int32_t* ci = nullptr;
+        double* val = nullptr;
+        const int64_t nnz = kern::synth_csr_device(e->s, rows, cols, density, seed, &rp, &ci, &val);
+        e->launches += 2;
+        finish_device_csr(e, rows, cols, nnz, rp, ci, val);
+        *out = e;
+    });
+    if (st != PLNMF_OK) release(e);
+    return st;
+}
+
+plnmf_status plnmf_gpu_create_mm(int32_t device, const plnmf_mm* m, int64_t rank, plnmf_gpu_engine** out) {
+    if (m && !plnmf::mm_coordinate(m)) {  // "array real general": a dense InputMatrix
+        if (!out) return guarded([] { throw std::invalid_argument("plnmf_gpu_create_mm: null output"); });
+        return plnmf_gpu_create_dense(device, plnmf::mm_nrows(m), plnmf::mm_ncols(m), plnmf::mm_values(m).data(),
+                                      rank, out);
+    }
+    plnmf_gpu_engine* e = nullptr;
+    const plnmf_status st = guarded([&] {
+        if (!m || !out) throw std::invalid_argument("plnmf_gpu_create_mm: null argument");
+        e = new plnmf_gpu_engine();
+        setup_common(e, device, rank);
+        int64_t* rp = nullptr;
+        int32_t* ci = nullptr;
+        double* val = nullptr;
+        const auto& v = plnmf::mm_values(m);
+        const int64_t nnz = kern::coo_to_csr_device(e->s, plnmf::mm_nrows(m), plnmf::mm_ncols(m), (int64_t)v.size(),
+                                                    plnmf::mm_rows(m).data(), plnmf::mm_cols(m).data(), v.data(),
+                                                    &rp, &ci, &val);
+        e->launches += 5;
+        finish_device_csr(e, plnmf::mm_nrows(m), plnmf::mm_ncols(m), nnz, rp, ci, val);
+        *out = e;
+    });
+    if (st != PLNMF_OK) release(e);
+    return st;
+}
+
+plnmf_status plnmf_gpu_get_csr(plnmf_gpu_engine* e, int64_t* row_ptr, int64_t* col_idx, double* values) {
+    return guarded([&] {
+        check_engine(e);
+        if (!e->sparse || e->shard) throw std::invalid_argument("plnmf_gpu_get_csr: not a sparse single engine");
+        if (row_ptr)
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(row_ptr, e->rp, sizeof(int64_t) * (e->v + 1), cudaMemcpyDeviceToHost, e->s));
+        std::vector<int32_t> ci32(col_idx ? std::max<int64_t>(1, e->nnz) : 0);
+        if (col_idx && e->nnz > 0)
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(ci32.data(), e->ci, sizeof(int32_t) * e->nnz, cudaMemcpyDeviceToHost, e->s));
+        if (values && e->nnz > 0)
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(values, e->val, sizeof(double) * e->nnz, cudaMemcpyDeviceToHost, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        if (col_idx)
+            for (int64_t i = 0; i < e->nnz; ++i) col_idx[i] = ci32[i];
+    });
+}
+
+plnmf_status plnmf_gpu_get_csr_rows(plnmf_gpu_engine* e, int32_t transposed, const int64_t* rows, int64_t n,
+                                    int64_t* row_ptr_out, int64_t* col_idx, double* values) {
+    return guarded([&] {
+        check_engine(e);
+        if (!e->sparse) throw std::invalid_argument("plnmf_gpu_get_csr_rows: not a sparse engine");
+        const int64_t* rp = transposed ? e->trp : e->rp;
+        const int32_t* ci = transposed ? e->tci : e->ci;
+        const double* val = transposed ? e->tval : e->val;
+        const int64_t nrows = transposed ? e->d : e->v;
+        if (n < 0 || (n > 0 && (!rows || !row_ptr_out))) throw std::invalid_argument("plnmf_gpu_get_csr_rows: bad argument");
+        row_ptr_out[0] = 0;
+        std::vector<int64_t> lo(n), hi(n);
+        for (int64_t i = 0; i < n; ++i) {
+            if (rows[i] < 0 || rows[i] >= nrows) throw std::invalid_argument("plnmf_gpu_get_csr_rows: row out of range");
+            int64_t b[2];
+            PLNMF_CUDA_CHECK(cudaMemcpy(b, rp + rows[i], sizeof(b), cudaMemcpyDeviceToHost));
+            lo[i] = b[0];
+            hi[i] = b[1];
+            row_ptr_out[i + 1] = row_ptr_out[i] + (b[1] - b[0]);
+        }
+        if (!col_idx && !values) return;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t cnt = hi[i] - lo[i];
+            if (cnt == 0) continue;
+            if (col_idx) {
+                std::vector<int32_t> c32(cnt);
+                PLNMF_CUDA_CHECK(cudaMemcpy(c32.data(), ci + lo[i], sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost));
+                for (int64_t j = 0; j < cnt; ++j) col_idx[row_ptr_out[i] + j] = c32[j];
+            }
+            if (values)
+                PLNMF_CUDA_CHECK(cudaMemcpy(values + row_ptr_out[i], val + lo[i], sizeof(double) * cnt,
+                                            cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+plnmf_status plnmf_gpu_get_rows(plnmf_gpu_engine* e, plnmf_buffer which, const int64_t* rows, int64_t n,
+                                double* out) {
+    return guarded([&] {
+        check_engine(e);
+        if (n < 0 || (n > 0 && (!rows || !out))) throw std::invalid_argument("plnmf_gpu_get_rows: bad argument");
+        const double* src = nullptr;
+        int64_t nr = 0;
+        switch (which) {
+            case PLNMF_BUF_W: src = e->w; nr = e->v; break;
+            case PLNMF_BUF_HT: src = e->ht; nr = e->d; break;
+            case PLNMF_BUF_P: src = e->p; nr = e->v; break;
+            case PLNMF_BUF_R: src = e->r; nr = e->d; break;
+            default: throw std::invalid_argument("plnmf_gpu_get_rows: W, HT, P or R expected");
+        }
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        for (int64_t i = 0; i < n; ++i) {
+            if (rows[i] < 0 || rows[i] >= nr) throw std::invalid_argument("plnmf_gpu_get_rows: row out of range");
+            PLNMF_CUDA_CHECK(cudaMemcpyAsync(out + i * e->k, src + rows[i] * e->k, sizeof(double) * e->k,
+                                             cudaMemcpyDeviceToHost, e->s));
+        }
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    });
 }
 
 plnmf_status plnmf_gpu_destroy(plnmf_gpu_engine* e) {
@@ -1022,11 +1203,38 @@ plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* c
         if (cfg->rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
         cudaEvent_t a = event_at(e, 0), b = event_at(e, 1);
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        // per-phase events on the engine stream (the stream every step's kernels are
+        // launched on; the Gram side stream joins it inside precompute_*), 5 per iteration
+        for (int64_t i = 0; i < 5 * n + 2; ++i) event_at(e, (size_t)i);
         PLNMF_CUDA_CHECK(cudaEventRecord(a, e->s));
-        for (int64_t i = 0; i < n; ++i) one_iteration(e, *cfg, alg);
+        for (int64_t i = 0; i < n; ++i) {
+            cudaEvent_t* ev = &e->events[(size_t)(2 + 5 * i)];
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[0], e->s));
+            precompute_h(e);
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[1], e->s));
+            update_h(e, *cfg, alg);
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[2], e->s));
+            precompute_w(e);
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[3], e->s));
+            update_w(e, *cfg, alg);
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[4], e->s));
+        }
         PLNMF_CUDA_CHECK(cudaEventRecord(b, e->s));
         PLNMF_CUDA_CHECK(cudaEventSynchronize(b));
         if (device_ms) *device_ms = elapsed_s(a, b) * 1e3;
+        double ph[4] = {0, 0, 0, 0};
+        for (int64_t i = 0; i < n; ++i) {
+            cudaEvent_t* ev = &e->events[(size_t)(2 + 5 * i)];
+            for (int j = 0; j < 4; ++j) ph[j] += elapsed_s(ev[j], ev[j + 1]) * 1e3;
+        }
+        for (int j = 0; j < 4; ++j) e->last_phase_ms[j] = ph[j];
+    });
+}
+
+plnmf_status plnmf_gpu_phase_ms(const plnmf_gpu_engine* e, double* out4) {
+    return guarded([&] {
+        if (!e || !out4) throw std::invalid_argument("plnmf_gpu_phase_ms: null argument");
+        for (int j = 0; j < 4; ++j) out4[j] = e->last_phase_ms[j];
     });
 }
 
@@ -1169,6 +1377,12 @@ plnmf_status plnmf_gpu_get_stats(const plnmf_gpu_engine* e, plnmf_gpu_stats* out
         if (!e || !out) throw std::invalid_argument("plnmf_gpu_get_stats: null argument");
         out->kernel_launches = e->launches;
         out->persistent_ctas = e->plan_w.grid;
+        auto code = [&](const kern::PhaseBPlan& pl) {
+            if (e->plan_tile < 0) return -1;
+            return pl.streaming ? 3 : pl.stage_ops ? 0 : pl.sqn_smem ? 1 : 2;
+        };
+        out->w_plan = code(e->plan_w);
+        out->h_plan = code(e->plan_h);
         out->sm_count = e->sms;
         out->device_bytes = e->bytes;
     });

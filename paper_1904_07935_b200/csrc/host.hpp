@@ -5,6 +5,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "plnmf_gpu.h"
 
@@ -13,8 +14,26 @@ namespace plnmf {
 void set_last_error(const std::string& msg);
 void validate_config(const plnmf_config& c);
 void init_factors_host(int64_t v, int64_t d, const plnmf_config& cfg, double* w, double* ht);
+// parsed Matrix Market file (mm.cpp)
+const std::vector<int64_t>& mm_rows(const plnmf_mm* m);
+const std::vector<int64_t>& mm_cols(const plnmf_mm* m);
+const std::vector<double>& mm_values(const plnmf_mm* m);
+bool mm_coordinate(const plnmf_mm* m);
+int64_t mm_nrows(const plnmf_mm* m);
+int64_t mm_ncols(const plnmf_mm* m);
 void synth_csr(int64_t rows, int64_t cols, double density, uint64_t seed, int64_t* row_ptr,
                int64_t* col_idx, double* values, int64_t* nnz);
+
+// Matrix Market parse failure (proj/include/plnmf/matrix_market.hpp:12-19):
+// "source:line: what", a std::runtime_error.
+class ParseError : public std::runtime_error {
+public:
+    ParseError(const std::string& source, int64_t line, const std::string& what);
+    int64_t line() const { return line_; }
+
+private:
+    int64_t line_ = 0;
+};
 
 // Non-finite objective (proj/src/solver.cpp:96-98 throws std::runtime_error).
 struct NonFinite : std::runtime_error {
@@ -41,6 +60,9 @@ plnmf_status guarded(F&& f) {
     } catch (const std::domain_error& e) {
         set_last_error(e.what());
         return PLNMF_DOMAIN;
+    } catch (const ParseError& e) {
+        set_last_error(e.what());
+        return PLNMF_PARSE;
     } catch (const DeviceError& e) {
         set_last_error(e.what());
         return PLNMF_CUDA;

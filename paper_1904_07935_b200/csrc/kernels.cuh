@@ -130,6 +130,16 @@ int direct_residual(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, con
                     const double* ht, double* partials, int64_t n_partials, double* out);
 int64_t direct_residual_partials(int64_t v, int64_t d);
 
+// ---- input construction on the device (ingest.cu) ---------------------------------
+// The synthetic CSR of plnmf_synth_csr generated on the device; returns nnz and
+// cudaMalloc'ed arrays (the caller owns them).
+int64_t synth_csr_device(cudaStream_t s, int64_t rows, int64_t cols, double density, uint64_t seed,
+                         int64_t** rp, int32_t** ci, double** val);
+// read_coordinate's assembly (matrix_market.cpp:147-172) of n host COO entries
+// (0-based, file order); returns nnz and cudaMalloc'ed CSR arrays.
+int64_t coo_to_csr_device(cudaStream_t s, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
+                          const int64_t* c, const double* v, int64_t** rp, int32_t** ci, double** val);
+
 // ---- layout / structure ------------------------------------------------------------
 // dst (rows x cols, row-major) := src (rows x cols, column-major), and back.
 int colmajor_to_rowmajor(cudaStream_t s, int64_t rows, int64_t cols, const double* src, double* dst);

@@ -51,7 +51,18 @@ class DeviceError(RuntimeError):
     """CUDA failure inside the engine (no reference counterpart)"""
 
 
-_STATUS = {1: InvalidArgument, 2: NonFiniteObjective, 3: DomainError, 4: DeviceError, 5: DeviceError}
+class ParseError(RuntimeError):
+    """plnmf::ParseError (proj/include/plnmf/matrix_market.hpp:12-19): "source:line: what" """
+
+    @property
+    def line(self) -> int:
+        try:
+            return int(str(self).rsplit(": ", 1)[0].rsplit(":", 1)[1])
+        except (IndexError, ValueError):
+            return 0
+
+
+_STATUS = {1: InvalidArgument, 2: NonFiniteObjective, 3: DomainError, 4: DeviceError, 5: DeviceError, 6: ParseError}
 
 
 def _check(status: int) -> None:
@@ -276,6 +287,39 @@ class _TraceBuf:
 _PRODUCT = {"p": 0, "q": 1, "r": 2, "s": 3, "column_norms": 4}
 
 
+class MatrixMarket:
+    """A parsed Matrix Market file (read_matrix_market, proj/src/matrix_market.cpp):
+    parsed on the host with the reference's rules and messages; the CSR is
+    assembled on the device when an engine is created from it."""
+
+    def __init__(self, path: Optional[str] = None, text: Optional[str] = None, source: str = "<string>"):
+        self._h = C.c_void_p()
+        if path is not None:
+            _check(L.lib().plnmf_mm_read(str(path).encode(), C.byref(self._h)))
+        else:
+            _check(L.lib().plnmf_mm_read_string(text.encode(), source.encode(), C.byref(self._h)))
+        r, c, n, sp = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        _check(L.lib().plnmf_mm_info(self._h, C.byref(r), C.byref(c), C.byref(n), C.byref(sp)))
+        self.rows, self.cols, self.entries, self.sparse = r.value, c.value, n.value, bool(sp.value)
+
+    def engine(self, rank: int, device: int = 0) -> "Engine":
+        h = C.c_void_p()
+        _check(L.lib().plnmf_gpu_create_mm(device, self._h, rank, C.byref(h)))
+        return Engine._adopt(h, rank)
+
+    def __del__(self):
+        try:
+            if self._h:
+                L.lib().plnmf_mm_free(self._h)
+        except Exception:
+            pass
+
+
+def read_matrix_market(path: str) -> MatrixMarket:
+    """proj/include/plnmf/matrix_market.hpp:25-29"""
+    return MatrixMarket(path=path)
+
+
 class Engine:
     """One device copy of A plus device-resident factors and workspace.
 
@@ -294,11 +338,55 @@ class Engine:
         else:
             d = a.dense()
             _check(lib.plnmf_gpu_create_dense(device, d.shape[0], d.shape[1], _f64p(d), rank, C.byref(self._h)))
+        self._info(rank)
+
+    def _info(self, rank):
         self.rank = rank
         r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
         n2 = C.c_double()
-        _check(lib.plnmf_gpu_input_info(self._h, C.byref(r), C.byref(c), C.byref(n), C.byref(n2)))
+        _check(L.lib().plnmf_gpu_input_info(self._h, C.byref(r), C.byref(c), C.byref(n), C.byref(n2)))
         self.v, self.d, self.nnz, self.norm_sq = r.value, c.value, n.value, n2.value
+
+    @classmethod
+    def _adopt(cls, handle, rank) -> "Engine":
+        eng = cls.__new__(cls)
+        eng._h = handle
+        eng._info(rank)
+        return eng
+
+    @classmethod
+    def synthetic(cls, rows: int, cols: int, density: float, seed: int, rank: int, device: int = 0) -> "Engine":
+        """An engine on the SURVEY.md 8(d) synthetic CSR generated on the device
+        (the stream of synth_csr; nothing of A is built on the host)."""
+        h = C.c_void_p()
+        _check(L.lib().plnmf_gpu_create_synthetic(device, rows, cols, float(density), int(seed), rank, C.byref(h)))
+        return cls._adopt(h, rank)
+
+    def get_csr(self) -> CsrMatrix:
+        rp = np.zeros(self.v + 1, np.int64)
+        ci = np.zeros(max(self.nnz, 1), np.int64)
+        val = np.zeros(max(self.nnz, 1))
+        _check(L.lib().plnmf_gpu_get_csr(self._h, _i64p(rp), _i64p(ci), _f64p(val)))
+        return CsrMatrix(self.v, self.d, rp, ci[: self.nnz], val[: self.nnz])
+
+    def get_csr_rows(self, rows, transposed: bool = False) -> CsrMatrix:
+        """The given rows of A (or of the device-built A^T) as a CSR."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        rp = np.zeros(len(rows) + 1, np.int64)
+        t = int(bool(transposed))
+        _check(L.lib().plnmf_gpu_get_csr_rows(self._h, t, _i64p(rows), len(rows), _i64p(rp), None, None))
+        ci = np.zeros(max(int(rp[-1]), 1), np.int64)
+        val = np.zeros(max(int(rp[-1]), 1))
+        _check(L.lib().plnmf_gpu_get_csr_rows(self._h, t, _i64p(rows), len(rows), _i64p(rp), _i64p(ci), _f64p(val)))
+        return CsrMatrix(len(rows), self.v if transposed else self.d, rp, ci[: rp[-1]], val[: rp[-1]])
+
+    def get_rows(self, name: str, rows) -> np.ndarray:
+        """Rows of W / Ht / P / R (len(rows) x K)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.zeros((len(rows), self.rank))
+        which = {"w": 0, "ht": 1, "p": 6, "r": 7}[name]
+        _check(L.lib().plnmf_gpu_get_rows(self._h, which, _i64p(rows), len(rows), _f64p(out)))
+        return out
 
     def close(self):
         if self._h:
@@ -394,6 +482,12 @@ class Engine:
         _check(L.lib().plnmf_gpu_run_iterations(self._h, C.byref(c), int(algorithm), n, C.byref(ms)))
         return ms.value
 
+    def phase_ms(self) -> dict:
+        """Device ms per step of the last run_iterations call (summed over its iterations)."""
+        out = np.zeros(4)
+        _check(L.lib().plnmf_gpu_phase_ms(self._h, _f64p(out)))
+        return dict(zip(("precompute_h", "update_h", "precompute_w", "update_w"), map(float, out)))
+
     def best_integer_tile(self, config: SolverConfig, candidates=None):
         """GPU counterpart of best_integer_tile (proj/src/cost_model.cpp:131-142):
         the candidate T whose tiled H + W update from the current factors is
@@ -419,7 +513,8 @@ class Engine:
         s = L.StatsC()
         _check(L.lib().plnmf_gpu_get_stats(self._h, C.byref(s)))
         return {"kernel_launches": int(s.kernel_launches), "persistent_ctas": int(s.persistent_ctas),
-                "sm_count": int(s.sm_count), "device_bytes": int(s.device_bytes)}
+                "sm_count": int(s.sm_count), "device_bytes": int(s.device_bytes),
+                "w_plan": int(s.w_plan), "h_plan": int(s.h_plan)}
 
     def synchronize(self) -> None:
         _check(L.lib().plnmf_gpu_synchronize(self._h))
