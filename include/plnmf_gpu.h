@@ -164,6 +164,8 @@ plnmf_status plnmf_mm_free(plnmf_mm* m);
 
 /* ---- engine -------------------------------------------------------------------- */
 int32_t plnmf_gpu_device_count(void);
+/* The device's name (cudaDeviceProp::name), NUL-terminated, truncated to len. */
+plnmf_status plnmf_gpu_device_name(int32_t device, char* buf, int32_t len);
 
 /* Uploads A (InputMatrix, proj/include/plnmf/input_matrix.hpp:11-34): validates
  * like CsrMatrix::validate (proj/src/csr_matrix.cpp:8-28), caches ||A||_F^2 in the

@@ -62,6 +62,7 @@ SIGNATURES = {
     "plnmf_gpu_get_csr_rows": (C.c_int, [Engine_p, i32, P_i64, i64, P_i64, P_i64, P_f64]),
     "plnmf_gpu_get_rows": (C.c_int, [Engine_p, C.c_int, P_i64, i64, P_f64]),
     "plnmf_gpu_device_count": (i32, []),
+    "plnmf_gpu_device_name": (C.c_int, [i32, C.c_char_p, i32]),
     "plnmf_gpu_create_csr": (C.c_int, [i32, i64, i64, i64, P_i64, P_i64, P_f64, i64, C.POINTER(Engine_p)]),
     "plnmf_gpu_create_dense": (C.c_int, [i32, i64, i64, P_f64, i64, C.POINTER(Engine_p)]),
     "plnmf_gpu_destroy": (C.c_int, [Engine_p]),

@@ -85,7 +85,26 @@ def build(verbose: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    build_cli()
     return LIB
+
+
+CLI = PKG / "plnmf-gpu"
+
+
+def build_cli() -> Path:
+    """The C++ command-line front end (csrc/cli/plnmf_gpu.cpp), linked against the
+    engine library through the C-ABI only (rpath: the package directory)."""
+    src = CSRC / "cli" / "plnmf_gpu.cpp"
+    deps = [src, ROOT / "include" / "plnmf_gpu.h", LIB]
+    if CLI.exists() and all(CLI.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return CLI
+    cmd = [_cxx(), "-O2", "-std=c++17", "-Wall", "-Wextra", f"-I{ROOT / 'include'}", str(src), "-o", str(CLI),
+           f"-L{PKG}", "-l:libplnmf_gpu.so", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"CLI build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return CLI
 
 
 def build_oracle() -> None:

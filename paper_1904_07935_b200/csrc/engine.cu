@@ -650,6 +650,15 @@ int32_t plnmf_gpu_device_count(void) {
     return n;
 }
 
+plnmf_status plnmf_gpu_device_name(int32_t device, char* buf, int32_t len) {
+    return guarded([&] {
+        if (!buf || len < 1) throw std::invalid_argument("plnmf_gpu_device_name: bad buffer");
+        cudaDeviceProp prop{};
+        PLNMF_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        std::snprintf(buf, (size_t)len, "%s", prop.name);
+    });
+}
+
 plnmf_status plnmf_gpu_create_csr(int32_t device, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
                                   const int64_t* col_idx, const double* values, int64_t rank,
                                   plnmf_gpu_engine** out) {
