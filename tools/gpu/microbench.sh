@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 o=gpurun_out/microbench.txt
 : > $o
-for b in latency_bench l2lat_bench pingpong_bench smem_bench exchange_bench2 chain_bench chain_bench2 cluster_probe; do
+for b in latency_bench l2lat_bench pingpong_bench smem_bench exchange_bench2 chain_bench cluster_probe; do
   echo "==== tools/$b.cu" >> $o; timeout 120 ./tools/$b.bin >> $o 2>&1
 done
 echo "==== tools/gemm_bench.cu (H shape: 416 threads, V=11314)" >> $o; timeout 120 ./tools/gemm_bench.bin 416 11314 >> $o 2>&1
