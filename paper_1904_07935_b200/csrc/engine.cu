@@ -38,7 +38,8 @@ struct plnmf_gpu_engine {
     bool ref_order = false;
     int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
     bool force_streaming = false;
-    double last_phase_ms[4] = {0, 0, 0, 0};  // run_iterations: precompute_h, update_h, precompute_w, update_w  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
+    double last_phase_ms[4] = {0, 0, 0, 0};
+  // run_iterations: precompute_h, update_h, precompute_w, update_w  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
 
     int64_t *rp = nullptr, *trp = nullptr;
     int32_t *ci = nullptr, *tci = nullptr;
@@ -166,54 +167,38 @@ void alloc_workspace(plnmf_gpu_engine* e) {
 }
 
 // ---- products ------------------------------------------------------------------------
-// R = A^T W on the main stream, S = W^T W on the side stream (skipped when the
-// last error evaluation already left gram(W) in S: same W, same deterministic
-// kernel, same bits — the reference recomputes it, proj/src/solver.cpp:34 vs
-// proj/src/hals.cpp:31).
+// R = A^T W then S = W^T W, one after the other on the engine stream (S is
+// skipped when the last error evaluation already left gram(W) in S: same W,
+// same deterministic kernel, same bits — the reference recomputes it,
+// proj/src/solver.cpp:34 vs proj/src/hals.cpp:31).  The two kernels are not
+// run concurrently: the SpMM is L2-gather bound and wants every SM's
+// registers for its loads in flight, the Gram is FP64-latency bound and
+// wants its own warps; side by side on two streams they took longer than
+// back to back (measured on the B200 at C2: P || Q 282 us vs P; Q 219 us).
 void precompute_h(plnmf_gpu_engine* e) {
     if (e->r_valid) {  // R was computed ahead, next to the last error evaluation
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join_r, 0));
         std::swap(e->r, e->r_next);
         e->r_valid = false;
-        if (e->s_valid) return;
-        e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
-        e->s_valid = true;
-        return;
-    }
-    const bool need_s = !e->s_valid;
-    if (need_s) {
-        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
-        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
-    }
-    // the SpMM is submitted first: its CTAs take the SMs' registers for their
-    // memory-level parallelism and the Gram's small CTAs fill what is left,
-    // so the two co-reside instead of the Gram draining the GPU first
-    if (e->sparse)
+    } else if (e->sparse) {
         e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->shard ? e->w_full : e->w,
                                       e->k, e->r, e->nnz_t);
-    else
+    } else {
         e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
-    if (need_s) e->launches += kern::gram(e->s2, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
-    if (need_s) {
-        PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
-        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
-        e->s_valid = true;
     }
+    if (e->s_valid) return;
+    e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
+    e->s_valid = true;
 }
 
-// P = A Ht (main stream), Q = Ht^T Ht (side stream).  The Gram scratch is
-// shared with S, which is never computed concurrently with Q.
+// P = A Ht then Q = Ht^T Ht (the Gram scratch is shared with S).
 void precompute_w(plnmf_gpu_engine* e) {
-    PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
-    PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
-    if (e->sparse)  // SpMM first, as in precompute_h
+    if (e->sparse)
         e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
                                       e->k, e->p, e->nnz);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
-    e->launches += kern::gram(e->s2, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
-    PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
-    PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
+    e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
 }
 
 void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
