@@ -62,7 +62,14 @@ typedef enum plnmf_math {
      * Gram-identity dots <P,W>, <S,Q> (serial, proj/src/metrics.cpp:104-115).
      * With it, iterate() trajectories are bit-identical to the reference's.
      * Column-stepped and slow (serial chains): not the production path. */
-    PLNMF_MATH_REFERENCE_ORDER = 2
+    PLNMF_MATH_REFERENCE_ORDER = 2,
+    /* EXACT, except that a DENSE input's products P = A Ht and R = A^T W
+     * (hals.cpp:29,43) run on the tensor cores: each fp64 operand row is
+     * scaled by a power of two and cut into six 8-bit digits, the 21 digit
+     * products that matter are exact u8 x u8 tcgen05.mma GEMMs with int32
+     * accumulators in TMEM, combined in fp64 (the Ozaki scheme; csrc/ozaki.cu).
+     * Relative error ~1e-14 per entry; not the reference's summation order. */
+    PLNMF_MATH_TENSOR = 3
 } plnmf_math;
 
 /* proj/include/plnmf/config.hpp:11-22 — SolverConfig, field for field. */

@@ -36,6 +36,11 @@ struct plnmf_gpu_engine {
     // Math::reference_order (PLNMF_MATH_REFERENCE_ORDER): exact arithmetic plus the
     // reference's own summation order for the W norms and the error dots (refmode.cu)
     bool ref_order = false;
+    // Math::tensor (dense A only): A's digit tiles for P = A Ht (rows of A) and for
+    // R = A^T W (columns of A), built once; the factor's digits per product
+    bool tensor = false;
+    uint8_t *dig_ap = nullptr, *dig_ar = nullptr, *dig_b = nullptr;
+    double *sc_ap = nullptr, *sc_ar = nullptr, *sc_b = nullptr, *oz_part = nullptr;
     int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
     bool force_streaming = false;
     double last_phase_ms[4] = {0, 0, 0, 0};
@@ -166,6 +171,38 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht, 0, sizeof(double) * d * k, e->s));
 }
 
+// ---- Math::tensor dense products (ozaki.cu) ----------------------------------------------
+void ensure_tensor(plnmf_gpu_engine* e) {
+    if (e->dig_ap) return;
+    const int nt = kern::ozaki_nt(e->k);
+    e->dig_ap = dalloc<uint8_t>(e, kern::ozaki_digit_bytes(e->v, e->d, 128));
+    e->dig_ar = dalloc<uint8_t>(e, kern::ozaki_digit_bytes(e->d, e->v, 128));
+    e->dig_b = dalloc<uint8_t>(e, std::max(kern::ozaki_digit_bytes(e->k, e->d, nt), kern::ozaki_digit_bytes(e->k, e->v, nt)));
+    e->sc_ap = dalloc<double>(e, e->v);
+    e->sc_ar = dalloc<double>(e, e->d);
+    e->sc_b = dalloc<double>(e, e->k);
+    e->oz_part = dalloc<double>(e, std::max(kern::ozaki_partial_doubles(e->v, e->k, e->d),
+                                            kern::ozaki_partial_doubles(e->d, e->k, e->v)));
+    e->launches += kern::ozaki_slice(e->s, e->v, e->d, e->a_dense, e->d, false, 128, e->sc_ap, e->dig_ap);
+    e->launches += kern::ozaki_slice(e->s, e->d, e->v, e->a_dense, e->d, true, 128, e->sc_ar, e->dig_ar);
+}
+
+// P = A Ht: left = A (V x D), right^T = Ht (D x K) -> right rows = Ht's columns
+void tensor_a_ht(plnmf_gpu_engine* e) {
+    ensure_tensor(e);
+    const int nt = kern::ozaki_nt(e->k);
+    e->launches += kern::ozaki_slice(e->s, e->k, e->d, e->ht, e->k, true, nt, e->sc_b, e->dig_b);
+    e->launches += kern::ozaki_gemm(e->s, e->v, e->k, e->d, e->dig_ap, e->sc_ap, e->dig_b, e->sc_b, e->oz_part, e->p);
+}
+
+// R = A^T W: left = A^T (D x V), right rows = W's columns
+void tensor_at_w(plnmf_gpu_engine* e) {
+    ensure_tensor(e);
+    const int nt = kern::ozaki_nt(e->k);
+    e->launches += kern::ozaki_slice(e->s, e->k, e->v, e->w, e->k, true, nt, e->sc_b, e->dig_b);
+    e->launches += kern::ozaki_gemm(e->s, e->d, e->k, e->v, e->dig_ar, e->sc_ar, e->dig_b, e->sc_b, e->oz_part, e->r);
+}
+
 // ---- products ------------------------------------------------------------------------
 // R = A^T W then S = W^T W, one after the other on the engine stream (S is
 // skipped when the last error evaluation already left gram(W) in S: same W,
@@ -183,6 +220,8 @@ void precompute_h(plnmf_gpu_engine* e) {
     } else if (e->sparse) {
         e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->shard ? e->w_full : e->w,
                                       e->k, e->r, e->nnz_t);
+    } else if (e->tensor) {
+        tensor_at_w(e);
     } else {
         e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
     }
@@ -196,6 +235,8 @@ void precompute_w(plnmf_gpu_engine* e) {
     if (e->sparse)
         e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
                                       e->k, e->p, e->nnz);
+    else if (e->tensor)
+        tensor_a_ht(e);
     else
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
     e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
@@ -858,10 +899,12 @@ plnmf_status plnmf_gpu_input_info(const plnmf_gpu_engine* e, int64_t* rows, int6
 plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
     return guarded([&] {
         check_engine(e);
-        if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED && math != PLNMF_MATH_REFERENCE_ORDER)
+        if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED && math != PLNMF_MATH_REFERENCE_ORDER &&
+            math != PLNMF_MATH_TENSOR)
             throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
         e->math = math == PLNMF_MATH_FUSED ? Math::fused : Math::exact;
         e->ref_order = math == PLNMF_MATH_REFERENCE_ORDER;
+        e->tensor = math == PLNMF_MATH_TENSOR && !e->sparse;  // sparse inputs have no dense GEMM
         e->s_valid = false;
         e->r_valid = false;
     });
@@ -1244,10 +1287,12 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
             switch (which) {
                 case 0:
                     if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p, e->nnz);
+                    else if (e->tensor) tensor_a_ht(e);
                     else e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
                     break;
                 case 1:
                     if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
+                    else if (e->tensor) tensor_at_w(e);
                     else e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
                     break;
                 case 2: e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms); break;

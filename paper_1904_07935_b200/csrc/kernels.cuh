@@ -50,6 +50,19 @@ int dense_a_ht(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const do
 int dense_at_w(cudaStream_t s, Math m, int64_t v, int64_t d, int64_t k, const double* a,
                const double* w, double* r);
 
+// ---- Math::tensor: Ozaki-split u8 tcgen05 GEMMs for dense A (ozaki.cu) -------------
+// Digit tiles of x(r, k) (rows x cols; base[r*ld + k], or base[k*ld + r] when trans)
+// with power-of-two row scales, in the GEMM's streaming layout (row tile rt).
+int64_t ozaki_digit_bytes(int64_t rows, int64_t cols, int rt);
+int ozaki_nt(int64_t n);  // the GEMM's N tile for n output columns
+int ozaki_slice(cudaStream_t s, int64_t rows, int64_t cols, const double* base, int64_t ld, bool trans, int rt,
+                double* scale, uint8_t* out);
+int64_t ozaki_partial_doubles(int64_t m, int64_t n, int64_t kdim);
+// out (m x n, row-major) := left (m x kdim) * right^T, both given as digit tiles
+// (left: row tile 128, right: row tile ozaki_nt(n)); part: ozaki_partial_doubles.
+int ozaki_gemm(cudaStream_t s, int64_t m, int64_t n, int64_t kdim, const uint8_t* a_digits, const double* sa,
+               const uint8_t* b_digits, const double* sb, double* part, double* out);
+
 // ---- tiled (PL-NMF) update, proj/src/tiled.cpp:176-214 --------------------------
 struct PhaseBPlan {
     int grid = 0;            // CTAs

@@ -88,6 +88,7 @@ class Math(enum.IntEnum):
     exact = 0  # separate rn multiply/add in the reference's order (bitwise where the order is shared)
     fused = 1  # fma in the same order
     reference_order = 2  # exact + the reference's own W-norm and error-dot order (bitwise trajectories)
+    tensor = 3  # exact, but dense-A products on the tensor cores (Ozaki u8 tcgen05 GEMMs)
 
 
 @dataclass

@@ -129,6 +129,18 @@ def test_c4_dense_20k_k160(gpu):
     assert rel_max(w, got2.w) <= 1e-10
     assert abs(tr2.records[0].rel_error - rtr["records"][0, 1]) <= 1e-12 * rtr["records"][0, 1]
 
+    # the tensor-core products (Ozaki u8 tcgen05, Math.tensor) against the exact ones
+    # (bit-identical to the reference's gemm) on the reference's iteration-1 state
+    exact = {}
+    for math in (P.Math.exact, P.Math.tensor):
+        eng.set_math(math)
+        eng.set_factors(P.FactorPair(w, ht))
+        eng.precompute_h_products()
+        eng.precompute_w_products()
+        exact[math] = (eng.get_product("r"), eng.get_product("p"))
+    for a0, a1 in zip(exact[P.Math.exact], exact[P.Math.tensor]):
+        assert np.max(np.abs(a1 - a0) / np.maximum(a0, 1e-300)) <= 1e-13
+
 
 # ------------------------------------------------------------------------------ C5
 def _compact(csr, fetch):
