@@ -15,8 +15,13 @@
 //   keeps the 21 digit products with i + j <= S + 1: each is an exact u8 x u8
 //   tensor-core GEMM accumulated in int32 in TMEM (one accumulator per level
 //   L, 6 x N columns), and the levels are combined in fp64 from the smallest.
-//   Relative error ~2^-46 per entry (non-negative data: no cancellation),
-//   against the reference's own sequential-sum rounding of ~sqrt(K) 2^-53.
+//   The error is bounded by the operand scales, not by the entry: every
+//   digit truncation leaves < 2^-48 of its row's (column's) maximum, so
+//   |C - C~|(i,j) <= n 2^-46 sa(i) sb(j) for reduction length n.  For
+//   well-scaled non-negative data (no cancellation) that is ~2^-46 relative
+//   per entry; an operand column whose entries span many decades (the
+//   collapsed columns right after iteration 1) keeps the
+//   bound, not the per-entry figure.
 //   The reduction dimension is split so no int32 accumulator can overflow
 //   (6 products per level x 5024 x 255^2 < 2^31); the splits' fp64 partials
 //   are added in split order.
