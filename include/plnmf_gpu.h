@@ -250,55 +250,64 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which,
                                    const double* in_colmajor);
 
 /* ---- sharded engine (multi-GPU) ------------------------------------
- * Rank g of a world owns the W rows [v_lo, v_hi) and the Ht rows [d_lo, d_hi):
- * it holds A's CSR row block A[v_lo:v_hi, :] (global column indices) and the
- * CSR of A^T's row block A^T[d_lo:d_hi, :] (global row indices, ascending —
- * transpose() order, proj/src/csr_matrix.cpp:30-50), plus full-size gather
- * buffers for W and Ht that the caller's collectives fill.  The products use
- * the gathered factor (R = A^T[d_lo:d_hi,:] W, P = A[v_lo:v_hi,:] Ht); the Gram
- * products are this rank's partials (the caller reduces them in rank order
- * and writes the total back).  The W update is driven column by column so the
- * caller can gather every rank's sum of squares between step and normalise.
- * ||A||_F^2 of the whole matrix is passed in. */
+ * One engine per GPU (one process per GPU, or several engines in one process).
+ * Rank g of `world` (<= 8) owns the W rows [v_lo, v_hi) and the Ht rows
+ * [d_lo, d_hi) of balanced contiguous splits (the first n % world ranks get one
+ * row more): A's CSR row block A[v_lo:v_hi, :] and the CSR of A^T's row block
+ * A^T[d_lo:d_hi, :] (global indices; entries of each A^T row in ascending source
+ * row, the order of transpose(), proj/src/csr_matrix.cpp:30-50).  After the ranks
+ * are connected, the ordinary step/loop calls (plnmf_gpu_iterate,
+ * plnmf_gpu_run_iterations, plnmf_gpu_precompute_*, plnmf_gpu_update_*,
+ * plnmf_gpu_evaluate_error, plnmf_gpu_{set,get,init}_factors) run the sharded
+ * iteration; every rank must make the same calls in the same order (they
+ * exchange data with each other on the device, over NVLink peer memory).
+ * Factors and products crossing the boundary are the rank's local rows;
+ * init_factors gives each rank its rows of the whole factors' stream
+ * (proj/src/solver.cpp:43-51).  Tiled algorithm only; Math::exact or fused. */
 typedef enum plnmf_buffer {
-    PLNMF_BUF_W = 0,         /* local W rows, row-major (v_hi-v_lo) x K */
-    PLNMF_BUF_HT = 1,        /* local Ht rows, row-major (d_hi-d_lo) x K */
-    PLNMF_BUF_W_FULL = 2,    /* gather buffer, row-major V x K */
-    PLNMF_BUF_HT_FULL = 3,   /* gather buffer, row-major D x K */
-    PLNMF_BUF_S = 4,         /* K x K */
-    PLNMF_BUF_Q = 5,         /* K x K */
-    PLNMF_BUF_P = 6,         /* local rows of P */
-    PLNMF_BUF_R = 7,         /* local rows of R */
-    PLNMF_BUF_COLUMN_SS = 8, /* 1 double: this rank's sum of squares of the last stepped column */
-    PLNMF_BUF_WORLD_SS = 9   /* world doubles: every rank's column sum of squares, rank order */
+    PLNMF_BUF_W = 0,  /* local W rows, row-major (v_hi-v_lo) x K */
+    PLNMF_BUF_HT = 1, /* local Ht rows, row-major (d_hi-d_lo) x K */
+    PLNMF_BUF_P = 6,  /* local rows of P */
+    PLNMF_BUF_R = 7   /* local rows of R */
 } plnmf_buffer;
 
-plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int64_t v, int64_t d, int64_t v_lo,
-                                    int64_t v_hi, int64_t d_lo, int64_t d_hi, int64_t nnz_rows,
-                                    const int64_t* rp_rows, const int64_t* ci_rows,
+#define PLNMF_IPC_HANDLE_BYTES 64
+
+/* A rank from host CSR blocks (global indices); a_norm_sq = ||A||_F^2 of the whole matrix. */
+plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int32_t shard_rank, int64_t v, int64_t d,
+                                    int64_t nnz_rows, const int64_t* rp_rows, const int64_t* ci_rows,
                                     const double* val_rows, int64_t nnz_cols, const int64_t* rp_cols,
                                     const int64_t* ci_cols, const double* val_cols, double a_norm_sq,
                                     int64_t rank, plnmf_gpu_engine** out);
-/* Device pointer and shape of an engine buffer (row-major fp64), for the caller's collectives. */
-plnmf_status plnmf_gpu_buffer(plnmf_gpu_engine* e, plnmf_buffer which, void** dev_ptr, int64_t* rows,
-                              int64_t* cols);
-/* Rows of an engine buffer (PLNMF_BUF_W, _HT, _P, _R; local rows on a shard):
- * out = n x K row-major, out[i*K + j] = buffer(rows[i], j).  For sampled parity
- * checks on inputs too large to download whole (C5). */
+/* A rank of the synthetic matrix of plnmf_synth_csr(v, d, density, seed), its blocks
+ * generated on the device (C5: nothing of A exists on the host).  ||A||^2 is then
+ * set with plnmf_gpu_shard_set_norm_sq (see plnmf_gpu_shard_norm_sq). */
+plnmf_status plnmf_gpu_create_shard_synthetic(int32_t device, int32_t world, int32_t shard_rank, int64_t v,
+                                              int64_t d, double density, uint64_t seed, int64_t rank,
+                                              plnmf_gpu_engine** out);
+plnmf_status plnmf_gpu_shard_info(const plnmf_gpu_engine* e, int32_t* world, int32_t* shard_rank, int64_t* v_lo,
+                                  int64_t* v_hi, int64_t* d_lo, int64_t* d_hi);
+/* InputMatrix's serial ||A||^2 (proj/src/input_matrix.cpp:15-20) continued from `start`
+ * over this rank's rows: chained rank 0 -> world-1 it reproduces the single sum exactly. */
+plnmf_status plnmf_gpu_shard_norm_sq(plnmf_gpu_engine* e, double start, double* out);
+plnmf_status plnmf_gpu_shard_set_norm_sq(plnmf_gpu_engine* e, double a_norm_sq);
+/* Connecting ranks in different processes: every rank exports its window's CUDA IPC
+ * handle (PLNMF_IPC_HANDLE_BYTES), the caller all-gathers them (any transport) and
+ * passes world handles in rank order. */
+plnmf_status plnmf_gpu_shard_ipc_handle(plnmf_gpu_engine* e, void* handle);
+plnmf_status plnmf_gpu_shard_connect(plnmf_gpu_engine* e, const void* handles);
+/* Connecting the ranks 0..world-1 of one process (any devices with peer access; several
+ * ranks may share one device, each then using an equal share of its SMs — that needs
+ * CUDA_MODULE_LOADING=EAGER in the process, else PLNMF_INVALID_ARGUMENT). */
+plnmf_status plnmf_gpu_shard_connect_local(plnmf_gpu_engine* const* engines, int32_t world);
+/* Failure detection: a device-side wait for another rank gives up after `seconds`
+ * (default 20) and the next synchronising call on this rank fails with PLNMF_CUDA
+ * ("a peer rank did not arrive ..."); the GPU is never left spinning. */
+plnmf_status plnmf_gpu_shard_set_timeout(plnmf_gpu_engine* e, double seconds);
+/* Rows of an engine buffer: out = n x K row-major, out[i*K + j] = buffer(rows[i], j).
+ * For sampled parity checks on inputs too large to download whole (C5). */
 plnmf_status plnmf_gpu_get_rows(plnmf_gpu_engine* e, plnmf_buffer which, const int64_t* rows, int64_t n,
                                 double* out);
-/* W_full[v_lo:v_hi] := W local; Ht_full[d_lo:d_hi] := Ht local (before the caller's gathers). */
-plnmf_status plnmf_gpu_shard_publish(plnmf_gpu_engine* e);
-/* Column-stepped tiled W update (tiled.cpp:176-193): begin = init + phase 1; per column t of
- * a tile: column_step (phase 2, writes COLUMN_SS), [caller gathers WORLD_SS], normalize; per
- * tile: phase3; end swaps the buffers. */
-plnmf_status plnmf_gpu_w_begin(plnmf_gpu_engine* e, const plnmf_config* cfg);
-plnmf_status plnmf_gpu_w_column_step(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t);
-plnmf_status plnmf_gpu_w_normalize(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t);
-plnmf_status plnmf_gpu_w_phase3(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t tile_begin);
-plnmf_status plnmf_gpu_w_end(plnmf_gpu_engine* e);
-/* <P, W> over the local rows (the caller sums the world's values in rank order). */
-plnmf_status plnmf_gpu_local_pw(plnmf_gpu_engine* e, double* out);
 
 /* ---- timing / instrumentation --------------------------------------------------- */
 /* n full iterations (H then W update, no error evaluation, no host sync inside),

@@ -83,16 +83,16 @@ SIGNATURES = {
     "plnmf_gpu_relative_error_direct": (C.c_int, [Engine_p, P_f64]),
     "plnmf_gpu_get_product": (C.c_int, [Engine_p, C.c_int, P_f64]),
     "plnmf_gpu_set_product": (C.c_int, [Engine_p, C.c_int, P_f64]),
-    "plnmf_gpu_create_shard": (C.c_int, [i32, i32, i64, i64, i64, i64, i64, i64, i64, P_i64, P_i64, P_f64, i64,
-                                         P_i64, P_i64, P_f64, f64, i64, C.POINTER(Engine_p)]),
-    "plnmf_gpu_buffer": (C.c_int, [Engine_p, C.c_int, C.POINTER(C.c_void_p), P_i64, P_i64]),
-    "plnmf_gpu_shard_publish": (C.c_int, [Engine_p]),
-    "plnmf_gpu_w_begin": (C.c_int, [Engine_p, P_cfg]),
-    "plnmf_gpu_w_column_step": (C.c_int, [Engine_p, P_cfg, i64]),
-    "plnmf_gpu_w_normalize": (C.c_int, [Engine_p, P_cfg, i64]),
-    "plnmf_gpu_w_phase3": (C.c_int, [Engine_p, P_cfg, i64]),
-    "plnmf_gpu_w_end": (C.c_int, [Engine_p]),
-    "plnmf_gpu_local_pw": (C.c_int, [Engine_p, P_f64]),
+    "plnmf_gpu_create_shard": (C.c_int, [i32, i32, i32, i64, i64, i64, P_i64, P_i64, P_f64, i64, P_i64, P_i64,
+                                         P_f64, f64, i64, C.POINTER(Engine_p)]),
+    "plnmf_gpu_create_shard_synthetic": (C.c_int, [i32, i32, i32, i64, i64, f64, u64, i64, C.POINTER(Engine_p)]),
+    "plnmf_gpu_shard_info": (C.c_int, [Engine_p, C.POINTER(i32), C.POINTER(i32), P_i64, P_i64, P_i64, P_i64]),
+    "plnmf_gpu_shard_norm_sq": (C.c_int, [Engine_p, f64, P_f64]),
+    "plnmf_gpu_shard_set_norm_sq": (C.c_int, [Engine_p, f64]),
+    "plnmf_gpu_shard_ipc_handle": (C.c_int, [Engine_p, C.c_void_p]),
+    "plnmf_gpu_shard_connect": (C.c_int, [Engine_p, C.c_void_p]),
+    "plnmf_gpu_shard_connect_local": (C.c_int, [C.POINTER(Engine_p), i32]),
+    "plnmf_gpu_shard_set_timeout": (C.c_int, [Engine_p, f64]),
     "plnmf_gpu_run_iterations": (C.c_int, [Engine_p, P_cfg, C.c_int, i64, P_f64]),
     "plnmf_gpu_phase_ms": (C.c_int, [Engine_p, P_f64]),
     "plnmf_gpu_time_kernel": (C.c_int, [Engine_p, P_cfg, i32, i32, P_f64]),

@@ -1,16 +1,13 @@
-// Column-stepped pieces of the tiled W update for the sharded (multi-GPU)
-// engine.  When W is row-sharded over ranks, column t's norm is a sum over
-// ALL ranks' rows (proj/src/tiled.cpp:129-146), so the update is driven from
-// the host one column at a time with a collective between the local
-// sum of squares and the normalisation:
+// Column-stepped pieces of the tiled W update, one launch per piece, for the
+// reference-order verification mode (Math::reference_order, refmode.cu /
+// engine.cu: update_w_reference_order), which forms each column's norm in the
+// reference's own summation order between the steps:
 //
-//   shard_col_step   phase 2 of column t for the local rows (tiled.cpp:103-128),
-//                    writes the clamped values and this rank's fixed-order
-//                    partial sum of squares (device scalar)
-//   shard_normalize  norm = sqrt(sum of the world's partials in rank order),
-//                    column t /= norm, clamp (tiled.cpp:137-146)
-//   shard_phase3     the tile's phase-3 rank-T update of the local rows
-//                    (tiled.cpp:158-174)
+//   shard_col_step   phase 2 of column t (tiled.cpp:103-128): writes the clamped
+//                    values and a fixed-order partial sum of squares
+//   shard_normalize  norm = sqrt(sum of the given partials in order), column t /=
+//                    norm, clamp (tiled.cpp:137-146)
+//   shard_phase3     the tile's phase-3 rank-T update (tiled.cpp:158-174)
 // Phase A (init + phase 1) is the streaming path's stream_phase_a.
 #include "common.cuh"
 #include "kernels.cuh"

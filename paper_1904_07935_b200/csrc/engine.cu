@@ -16,98 +16,20 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
-#include "host.hpp"
-#include "kernels.cuh"
-#include "plnmf_gpu.h"
+#include "engine.hpp"
 
 using plnmf::Math;
 namespace kern = plnmf::kern;
 
-struct plnmf_gpu_engine {
-    int device = 0;
-    cudaStream_t s = nullptr, s2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    int64_t v = 0, d = 0, k = 0, nnz = 0;
-    int64_t nnz_t = -1;  // nonzeros of the A^T block (sharded engines: of the local column block)
-    bool sparse = true;
-    double a2 = 0.0;
-    Math math = Math::exact;
-    // Math::reference_order (PLNMF_MATH_REFERENCE_ORDER): exact arithmetic plus the
-    // reference's own summation order for the W norms and the error dots (refmode.cu)
-    bool ref_order = false;
-    // Math::tensor (dense A only): A's digit tiles for P = A Ht (rows of A) and for
-    // R = A^T W (columns of A), built once; the factor's digits per product
-    bool tensor = false;
-    uint8_t *dig_ap = nullptr, *dig_ar = nullptr, *dig_b = nullptr;
-    double *sc_ap = nullptr, *sc_ar = nullptr, *sc_b = nullptr, *oz_part = nullptr;
-    int ref_threads = 1;  // the reference's OpenMP team size for the tiled norm partials
-    bool force_streaming = false;
-    double last_phase_ms[4] = {0, 0, 0, 0};
-  // run_iterations: precompute_h, update_h, precompute_w, update_w  // plnmf_gpu_force_streaming: tiled updates take the streaming plan
-
-    int64_t *rp = nullptr, *trp = nullptr;
-    int32_t *ci = nullptr, *tci = nullptr;
-    double *val = nullptr, *tval = nullptr, *a_dense = nullptr;
-    double *w = nullptr, *ht = nullptr, *w_new = nullptr, *h_new = nullptr;
-    double *p = nullptr, *q = nullptr, *r = nullptr, *sm = nullptr, *norms = nullptr;
-    double* r_next = nullptr;  // R of the current W computed ahead (iterate), swapped into r when used
-    double *gram_scratch = nullptr, *partials = nullptr, *dot_partials = nullptr;
-    double *scalars = nullptr;  // [0] pw, [1] sq, [2..4] error report, [5] direct sum
-    double *staging = nullptr, *direct_partials = nullptr;
-    double* host_scalars = nullptr;  // pinned mirror of scalars
-    unsigned* counters = nullptr;  // K, grid-exchange arrival counters
-    double* totals = nullptr;      // K, grid-exchange published norms
-    int64_t n_partials = 0, n_direct_partials = 0;
-
-    bool s_valid = false;  // sm == gram(w) of the current w
-    bool r_valid = false;  // r == A^T w of the current w, computed ahead on s2 (iterate: join_r)
-    cudaEvent_t join_r = nullptr;
-    uint64_t launches = 0, update_macs = 0;
-    int64_t bytes = 0;
-    int sms = 0;
-    std::vector<void*> allocs;
-
-    // cached phase-B plans, keyed by tile size
-    int64_t plan_tile = -1;
-    kern::PhaseBPlan plan_w, plan_h, plan_ref_w;
-    bool have_ref_w = false;
-
-
-    std::vector<cudaEvent_t> events;  // per-phase timing pool
-    long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
-    int64_t prof_n = 0;
-    double* qpanel = nullptr;         // coeff column panels of the tiled updates
-    int64_t qpanel_n = 0;
-
-    // sharded engine (multi-GPU): local rows [v_lo, v_lo+v) of W and [d_lo, d_lo+d) of Ht
-    bool shard = false;
-    int world = 1;
-    int64_t vfull = 0, dfull = 0, v_lo = 0, d_lo = 0;
-    double *w_full = nullptr, *ht_full = nullptr;           // gather buffers (row-major V x K, D x K)
-    double *col_ss = nullptr, *world_ss = nullptr, *col_partials = nullptr;
-};
-
-namespace {
-
-using plnmf::DeviceError;
-using plnmf::guarded;
-
-template <class T>
-T* dalloc(plnmf_gpu_engine* e, int64_t n) {
-    void* ptr = nullptr;
-    const size_t bytes = sizeof(T) * (size_t)(n > 0 ? n : 1);
-    PLNMF_CUDA_CHECK(cudaMalloc(&ptr, bytes));
-    e->allocs.push_back(ptr);
-    e->bytes += (int64_t)bytes;
-    return static_cast<T*>(ptr);
-}
+namespace plnmf {
+namespace eng {
 
 void release(plnmf_gpu_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
     if (e->s) cudaStreamSynchronize(e->s);
     if (e->s2) cudaStreamSynchronize(e->s2);
+    if (e->shard) shard::close_peers(e);
     for (void* ptr : e->allocs) cudaFree(ptr);
     if (e->host_scalars) cudaFreeHost(e->host_scalars);
     for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
@@ -141,12 +63,17 @@ void setup_common(plnmf_gpu_engine* e, int device, int64_t rank) {
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join_r, cudaEventDisableTiming));
 }
 
+// The workspace (UpdateWorkspace, proj/include/plnmf/workspace.hpp:15-55).  A
+// sharded engine's factor buffers are slices of its peer window (set up by
+// shard_engine.cu before this call).
 void alloc_workspace(plnmf_gpu_engine* e) {
     const int64_t v = e->v, d = e->d, k = e->k;
-    e->w = dalloc<double>(e, v * k);
-    e->w_new = dalloc<double>(e, v * k);
-    e->ht = dalloc<double>(e, d * k);
-    e->h_new = dalloc<double>(e, d * k);
+    if (!e->shard) {
+        e->w = dalloc<double>(e, v * k);
+        e->w_new = dalloc<double>(e, v * k);
+        e->ht = dalloc<double>(e, d * k);
+        e->h_new = dalloc<double>(e, d * k);
+    }
     e->p = dalloc<double>(e, v * k);
     e->r = dalloc<double>(e, d * k);
     e->r_next = dalloc<double>(e, d * k);
@@ -167,9 +94,21 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->r, 0, sizeof(double) * d * k, e->s));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->q, 0, sizeof(double) * k * k, e->s));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->sm, 0, sizeof(double) * k * k, e->s));
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->w, 0, sizeof(double) * v * k, e->s));
-    PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht, 0, sizeof(double) * d * k, e->s));
+    if (!e->shard) {
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->w, 0, sizeof(double) * v * k, e->s));
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht, 0, sizeof(double) * d * k, e->s));
+    }
 }
+
+}  // namespace eng
+}  // namespace plnmf
+
+namespace {
+
+using plnmf::DeviceError;
+using plnmf::dalloc;
+using plnmf::guarded;
+using namespace plnmf::eng;
 
 // ---- Math::tensor dense products (ozaki.cu) ----------------------------------------------
 void ensure_tensor(plnmf_gpu_engine* e) {
@@ -218,8 +157,12 @@ void precompute_h(plnmf_gpu_engine* e) {
         std::swap(e->r, e->r_next);
         e->r_valid = false;
     } else if (e->sparse) {
-        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->shard ? e->w_full : e->w,
-                                      e->k, e->r, e->nnz_t);
+        const double* w = e->w;
+        if (e->shard) {  // every rank's W rows have arrived in this rank's window
+            plnmf::shard::wait(e, plnmf::kChanW);
+            w = plnmf::shard::w_full(e);
+        }
+        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, w, e->k, e->r, e->nnz_t);
     } else if (e->tensor) {
         tensor_at_w(e);
     } else {
@@ -227,24 +170,41 @@ void precompute_h(plnmf_gpu_engine* e) {
     }
     if (e->s_valid) return;
     e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
+    if (e->shard) plnmf::shard::reduce_kxk(e, plnmf::kChanS, e->sm);  // S = sum of the ranks' partials
     e->s_valid = true;
 }
 
 // P = A Ht then Q = Ht^T Ht (the Gram scratch is shared with S).
 void precompute_w(plnmf_gpu_engine* e) {
-    if (e->sparse)
-        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->shard ? e->ht_full : e->ht,
-                                      e->k, e->p, e->nnz);
-    else if (e->tensor)
+    if (e->sparse) {
+        const double* ht = e->ht;
+        if (e->shard) {
+            plnmf::shard::wait(e, plnmf::kChanHt);
+            ht = plnmf::shard::ht_full(e);
+        }
+        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, ht, e->k, e->p, e->nnz);
+    } else if (e->tensor) {
         tensor_a_ht(e);
-    else
+    } else {
         e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
+    }
     e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
+    if (e->shard) plnmf::shard::reduce_kxk(e, plnmf::kChanQ, e->q);
 }
 
 void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
     if (e->plan_tile == tile) return;
-    e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device, e->force_streaming);
+    if (e->shard) {
+        // the sharded W update is the streaming kernel with the cross-rank norm exchange
+        e->plan_w = kern::plan_stream_update(e->v, e->k, tile, true, e->device);
+        if (e->sm_cap > 0 && e->sm_cap < e->plan_w.grid) {  // ranks sharing one GPU
+            e->plan_w.grid = e->sm_cap;
+            e->plan_w.cooperative = false;
+            e->plan_w.rows_per_cta = e->v > 0 ? (e->v + e->sm_cap - 1) / e->sm_cap : 1;
+        }
+    } else {
+        e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device, e->force_streaming);
+    }
     e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device, e->force_streaming);
     const int64_t qn = kern::qpanel_doubles(e->k, tile);
     if (qn > e->qpanel_n) {
@@ -321,6 +281,7 @@ void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         e->launches += kern::reference_update_h(e->s, e->math, e->d, e->k, cfg.epsilon, e->ht, e->r, e->sm);
         e->update_macs += (uint64_t)e->d * e->k * e->k;
     }
+    if (e->shard) plnmf::shard::push_factor(e, plnmf::kChanHt);  // this rank's new Ht rows to every rank
 }
 
 // The W update with the reference's norm order (Math::reference_order): column
@@ -360,8 +321,27 @@ void update_w_reference_order(plnmf_gpu_engine* e, const plnmf_config& cfg, plnm
     e->r_valid = false;
 }
 
+// The sharded W update: the streaming kernel on the local
+// rows, every column's norm exchanged with the other ranks inside the kernel
+// (peer.cuh), then the new rows pushed into every rank's window.
+void update_w_shard(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    if (alg != PLNMF_ALGORITHM_TILED)
+        throw std::invalid_argument("sharded engine: the W update is sharded for the tiled algorithm only");
+    check_tile(cfg, e->k);
+    ensure_plans(e, cfg.tile_size);
+    const plnmf::WorldXch x = plnmf::shard::next_exchange(e);
+    e->launches += kern::stream_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true, e->w,
+                                       e->w_new, e->q, e->p, e->norms, e->partials, e->counters, &x);
+    std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
+    e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);
+    plnmf::shard::push_factor(e, plnmf::kChanW);
+    e->s_valid = false;
+    e->r_valid = false;
+}
+
 void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
-    if (e->ref_order && !e->shard) return update_w_reference_order(e, cfg, alg);
+    if (e->shard) return update_w_shard(e, cfg, alg);
+    if (e->ref_order) return update_w_reference_order(e, cfg, alg);
     if (alg == PLNMF_ALGORITHM_TILED) {
         check_tile(cfg, e->k);
         ensure_plans(e, cfg.tile_size);
@@ -394,15 +374,24 @@ struct ErrorReport {
 
 ErrorReport direct_error(plnmf_gpu_engine* e) {
     if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_direct: zero input matrix");
-    const int64_t np = kern::direct_residual_partials(e->v, e->d);
+    const int64_t np = kern::direct_residual_partials(e->v, e->shard ? e->world * e->dcap : e->d);
     if (np > e->n_direct_partials) {
         e->direct_partials = dalloc<double>(e, np);
         e->n_direct_partials = np;
     }
-    e->launches += kern::direct_residual(e->s, e->math, e->v, e->d, e->k, e->rp, e->ci, e->val, e->a_dense, e->w,
-                                         e->ht, e->direct_partials, np, e->scalars + 5);
+    if (e->shard) {  // this rank's rows of A - W Ht^T against the gathered Ht, summed over ranks
+        plnmf::shard::wait(e, plnmf::kChanHt);
+        e->launches += kern::direct_residual(e->s, e->math, e->v, e->world * e->dcap, e->k, e->rp, e->ci, e->val,
+                                             nullptr, e->w, plnmf::shard::ht_full(e), e->direct_partials, np,
+                                             e->scalars + 5);
+        plnmf::shard::reduce_scalar(e, e->scalars + 5);
+    } else {
+        e->launches += kern::direct_residual(e->s, e->math, e->v, e->d, e->k, e->rp, e->ci, e->val, e->a_dense, e->w,
+                                             e->ht, e->direct_partials, np, e->scalars + 5);
+    }
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 5, e->scalars + 5, sizeof(double), cudaMemcpyDeviceToHost, e->s));
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    if (e->shard) plnmf::shard::check_error(e);
     ErrorReport rep;
     rep.frob = e->host_scalars[5];
     rep.rel = std::sqrt(rep.frob / e->a2);
@@ -416,7 +405,9 @@ ErrorReport direct_error(plnmf_gpu_engine* e) {
 // after the reductions).
 ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
     if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_gram: zero input norm");
+    if (!(e->a2 == e->a2)) throw std::invalid_argument("sharded engine: ||A||^2 not set (plnmf_gpu_shard_set_norm_sq)");
     e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
+    if (e->shard) plnmf::shard::reduce_kxk(e, plnmf::kChanS, e->sm);
     e->s_valid = true;
     if (ahead_r) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
@@ -430,11 +421,13 @@ ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
         e->launches += kern::serial_dot_colmajor(e->s, e->k, e->k, e->sm, e->q, e->scalars + 1);
     } else {
         e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
+        if (e->shard) plnmf::shard::reduce_scalar(e, e->scalars + 0);  // <P, W> over all ranks' rows
         e->launches += kern::dot(e->s, e->math, e->k * e->k, e->sm, e->q, e->dot_partials, e->scalars + 1);
     }
     e->launches += kern::error_finalize(e->s, e->a2, e->scalars + 0, e->scalars + 1, e->scalars + 2);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 2, e->scalars + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->s));
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    if (e->shard) plnmf::shard::check_error(e);
     ErrorReport rep;
     rep.frob = e->host_scalars[2];
     rep.rel = e->host_scalars[3];
@@ -458,6 +451,10 @@ void set_factors(plnmf_gpu_engine* e, const double* w, const double* ht) {
     if (!w || !ht) throw std::invalid_argument("set_factors: null factor");
     upload_factor(e, w, e->v, e->w);
     upload_factor(e, ht, e->d, e->ht);
+    if (e->shard) {  // a sharded engine's local rows go to every rank's window
+        plnmf::shard::push_factor(e, plnmf::kChanW);
+        plnmf::shard::push_factor(e, plnmf::kChanHt);
+    }
     PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
     e->s_valid = false;
     e->r_valid = false;
@@ -902,6 +899,8 @@ plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
         if (math != PLNMF_MATH_EXACT && math != PLNMF_MATH_FUSED && math != PLNMF_MATH_REFERENCE_ORDER &&
             math != PLNMF_MATH_TENSOR)
             throw std::invalid_argument("plnmf_gpu_set_math: unknown mode");
+        if (e->shard && (math == PLNMF_MATH_REFERENCE_ORDER || math == PLNMF_MATH_TENSOR))
+            throw std::invalid_argument("plnmf_gpu_set_math: a sharded engine runs Math::exact or Math::fused");
         e->math = math == PLNMF_MATH_FUSED ? Math::fused : Math::exact;
         e->ref_order = math == PLNMF_MATH_REFERENCE_ORDER;
         e->tensor = math == PLNMF_MATH_TENSOR && !e->sparse;  // sparse inputs have no dense GEMM
@@ -940,6 +939,17 @@ plnmf_status plnmf_gpu_init_factors(plnmf_gpu_engine* e, const plnmf_config* cfg
         check_engine(e);
         if (!cfg) throw std::invalid_argument("plnmf_gpu_init_factors: null config");
         if (cfg->rank != e->k) throw std::invalid_argument("init_factors: rank does not match the engine");
+        if (e->shard) {  // the whole factors' stream (solver.cpp:43-51), this rank's rows of it
+            std::vector<double> w((size_t)(e->vfull * e->k)), ht((size_t)(e->dfull * e->k));
+            plnmf::init_factors_host(e->vfull, e->dfull, *cfg, w.data(), ht.data());
+            std::vector<double> wl((size_t)(e->v * e->k)), hl((size_t)(e->d * e->k));
+            for (int64_t j = 0; j < e->k; ++j) {
+                std::memcpy(&wl[(size_t)(j * e->v)], &w[(size_t)(j * e->vfull + e->v_lo)], sizeof(double) * e->v);
+                std::memcpy(&hl[(size_t)(j * e->d)], &ht[(size_t)(j * e->dfull + e->d_lo)], sizeof(double) * e->d);
+            }
+            set_factors(e, wl.data(), hl.data());
+            return;
+        }
         std::vector<double> w((size_t)(e->v * e->k)), ht((size_t)(e->d * e->k));
         plnmf::init_factors_host(e->v, e->d, *cfg, w.data(), ht.data());
         set_factors(e, w.data(), ht.data());
@@ -965,12 +975,18 @@ plnmf_status plnmf_gpu_iterate_host(plnmf_gpu_engine* e, const plnmf_config* cfg
     });
 }
 
+// step calls finish on the host; a sharded rank also reports a peer that never arrived
+static void finish_step(plnmf_gpu_engine* e) {
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    if (e->shard) plnmf::shard::check_error(e);
+}
+
 plnmf_status plnmf_gpu_precompute_h_products(plnmf_gpu_engine* e) {
-    return guarded([&] { check_engine(e); precompute_h(e); PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s)); });
+    return guarded([&] { check_engine(e); precompute_h(e); finish_step(e); });
 }
 
 plnmf_status plnmf_gpu_precompute_w_products(plnmf_gpu_engine* e) {
-    return guarded([&] { check_engine(e); precompute_w(e); PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s)); });
+    return guarded([&] { check_engine(e); precompute_w(e); finish_step(e); });
 }
 
 plnmf_status plnmf_gpu_update_h(plnmf_gpu_engine* e, const plnmf_config* cfg, plnmf_algorithm alg) {
@@ -978,7 +994,7 @@ plnmf_status plnmf_gpu_update_h(plnmf_gpu_engine* e, const plnmf_config* cfg, pl
         check_engine(e);
         if (!cfg) throw std::invalid_argument("plnmf_gpu_update_h: null config");
         update_h(e, *cfg, alg);
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        finish_step(e);
     });
 }
 
@@ -987,7 +1003,7 @@ plnmf_status plnmf_gpu_update_w(plnmf_gpu_engine* e, const plnmf_config* cfg, pl
         check_engine(e);
         if (!cfg) throw std::invalid_argument("plnmf_gpu_update_w: null config");
         update_w(e, *cfg, alg);
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+        finish_step(e);
     });
 }
 
@@ -1048,179 +1064,6 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which, con
     });
 }
 
-// ---- sharded engine --------------------------------------------------------------------
-plnmf_status plnmf_gpu_create_shard(int32_t device, int32_t world, int64_t v, int64_t d, int64_t v_lo, int64_t v_hi,
-                                    int64_t d_lo, int64_t d_hi, int64_t nnz_rows, const int64_t* rp_rows,
-                                    const int64_t* ci_rows, const double* val_rows, int64_t nnz_cols,
-                                    const int64_t* rp_cols, const int64_t* ci_cols, const double* val_cols,
-                                    double a_norm_sq, int64_t rank, plnmf_gpu_engine** out) {
-    plnmf_gpu_engine* e = nullptr;
-    const plnmf_status st = guarded([&] {
-        if (!out) throw std::invalid_argument("plnmf_gpu_create_shard: null output");
-        if (world < 1) throw std::invalid_argument("plnmf_gpu_create_shard: world must be >= 1");
-        if (v_lo < 0 || v_hi < v_lo || v_hi > v || d_lo < 0 || d_hi < d_lo || d_hi > d)
-            throw std::invalid_argument("plnmf_gpu_create_shard: shard ranges out of bounds");
-        const int64_t vl = v_hi - v_lo, dl = d_hi - d_lo;
-        validate_csr(vl, d, nnz_rows, rp_rows, ci_rows, val_rows);
-        validate_csr(dl, v, nnz_cols, rp_cols, ci_cols, val_cols);
-        if (d > INT32_MAX || v > INT32_MAX) throw std::invalid_argument("plnmf_gpu_create_shard: dimensions exceed int32");
-        e = new plnmf_gpu_engine();
-        setup_common(e, device, rank);
-        e->shard = true;
-        e->world = world;
-        e->vfull = v;
-        e->dfull = d;
-        e->v_lo = v_lo;
-        e->d_lo = d_lo;
-        e->v = vl;
-        e->d = dl;
-        e->nnz = nnz_rows;
-        e->nnz_t = nnz_cols;
-        e->sparse = true;
-        e->a2 = a_norm_sq;
-        auto upload = [&](int64_t rows, int64_t nnz, const int64_t* rp, const int64_t* ci, const double* val,
-                          int64_t*& drp, int32_t*& dci, double*& dval) {
-            std::vector<int32_t> ci32(nnz > 0 ? nnz : 1);
-            for (int64_t i = 0; i < nnz; ++i) ci32[i] = (int32_t)ci[i];
-            drp = dalloc<int64_t>(e, rows + 1);
-            dci = dalloc<int32_t>(e, nnz);
-            dval = dalloc<double>(e, nnz);
-            PLNMF_CUDA_CHECK(cudaMemcpy(drp, rp, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice));
-            if (nnz > 0) {
-                PLNMF_CUDA_CHECK(cudaMemcpy(dci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-                PLNMF_CUDA_CHECK(cudaMemcpy(dval, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
-            }
-        };
-        upload(vl, nnz_rows, rp_rows, ci_rows, val_rows, e->rp, e->ci, e->val);
-        upload(dl, nnz_cols, rp_cols, ci_cols, val_cols, e->trp, e->tci, e->tval);
-        alloc_workspace(e);
-        e->w_full = dalloc<double>(e, v * rank);
-        e->ht_full = dalloc<double>(e, d * rank);
-        e->col_ss = dalloc<double>(e, 1);
-        e->world_ss = dalloc<double>(e, world);
-        e->col_partials = dalloc<double>(e, 512);
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->w_full, 0, sizeof(double) * v * rank, e->s));
-        PLNMF_CUDA_CHECK(cudaMemsetAsync(e->ht_full, 0, sizeof(double) * d * rank, e->s));
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-        *out = e;
-    });
-    if (st != PLNMF_OK) release(e);
-    return st;
-}
-
-plnmf_status plnmf_gpu_buffer(plnmf_gpu_engine* e, plnmf_buffer which, void** ptr, int64_t* rows, int64_t* cols) {
-    return guarded([&] {
-        check_engine(e);
-        double* p = nullptr;
-        int64_t r = 0, c = e->k;
-        switch (which) {
-            case PLNMF_BUF_W: p = e->w; r = e->v; break;
-            case PLNMF_BUF_HT: p = e->ht; r = e->d; break;
-            case PLNMF_BUF_W_FULL: p = e->w_full; r = e->vfull; break;
-            case PLNMF_BUF_HT_FULL: p = e->ht_full; r = e->dfull; break;
-            case PLNMF_BUF_S: p = e->sm; r = e->k; break;
-            case PLNMF_BUF_Q: p = e->q; r = e->k; break;
-            case PLNMF_BUF_P: p = e->p; r = e->v; break;
-            case PLNMF_BUF_R: p = e->r; r = e->d; break;
-            case PLNMF_BUF_COLUMN_SS: p = e->col_ss; r = 1; c = 1; break;
-            case PLNMF_BUF_WORLD_SS: p = e->world_ss; r = e->world; c = 1; break;
-            default: throw std::invalid_argument("plnmf_gpu_buffer: unknown buffer");
-        }
-        if (!p) throw std::invalid_argument("plnmf_gpu_buffer: buffer not available (not a sharded engine?)");
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-        if (ptr) *ptr = p;
-        if (rows) *rows = r;
-        if (cols) *cols = c;
-    });
-}
-
-plnmf_status plnmf_gpu_shard_publish(plnmf_gpu_engine* e) {
-    return guarded([&] {
-        check_engine(e);
-        if (!e->shard) throw std::invalid_argument("plnmf_gpu_shard_publish: not a sharded engine");
-        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->w_full + e->v_lo * e->k, e->w, sizeof(double) * e->v * e->k,
-                                         cudaMemcpyDeviceToDevice, e->s));
-        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->ht_full + e->d_lo * e->k, e->ht, sizeof(double) * e->d * e->k,
-                                         cudaMemcpyDeviceToDevice, e->s));
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-        e->s_valid = false;
-    e->r_valid = false;
-    });
-}
-
-static void check_tiled(plnmf_gpu_engine* e, const plnmf_config* cfg) {
-    check_engine(e);
-    if (!cfg) throw std::invalid_argument("plnmf_gpu_w_*: null config");
-    plnmf::validate_config(*cfg);
-    if (cfg->rank != e->k) throw std::invalid_argument("iterate: factor dimensions do not match input and rank");
-    check_tile(*cfg, e->k);
-}
-
-plnmf_status plnmf_gpu_w_begin(plnmf_gpu_engine* e, const plnmf_config* cfg) {
-    return guarded([&] {
-        check_tiled(e, cfg);
-        e->launches += kern::stream_phase_a(e->s, e->math, e->v, e->k, cfg->tile_size, true, e->w, e->q, e->w_new);
-    });
-}
-
-plnmf_status plnmf_gpu_w_column_step(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t) {
-    return guarded([&] {
-        check_tiled(e, cfg);
-        if (t < 0 || t >= e->k) throw std::invalid_argument("plnmf_gpu_w_column_step: column out of range");
-        if (!e->col_partials) {
-            e->col_ss = dalloc<double>(e, 1);
-            e->world_ss = dalloc<double>(e, std::max(1, e->world));
-            e->col_partials = dalloc<double>(e, 512);
-        }
-        const int64_t b = (t / cfg->tile_size) * cfg->tile_size, en = std::min(e->k, b + cfg->tile_size);
-        e->launches += kern::shard_col_step(e->s, e->math, e->v, e->k, b, en, t, cfg->epsilon, e->w, e->w_new, e->q,
-                                            e->p, e->col_partials, e->col_ss);
-    });
-}
-
-plnmf_status plnmf_gpu_w_normalize(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t t) {
-    return guarded([&] {
-        check_tiled(e, cfg);
-        if (t < 0 || t >= e->k) throw std::invalid_argument("plnmf_gpu_w_normalize: column out of range");
-        if (!e->shard) {  // single engine: this rank's partial is the world
-            PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->world_ss, e->col_ss, sizeof(double), cudaMemcpyDeviceToDevice, e->s));
-        }
-        e->launches += kern::shard_normalize(e->s, e->v, e->k, t, cfg->epsilon, e->shard ? e->world : 1, e->world_ss,
-                                             e->w_new, e->norms);
-    });
-}
-
-plnmf_status plnmf_gpu_w_phase3(plnmf_gpu_engine* e, const plnmf_config* cfg, int64_t tile_begin) {
-    return guarded([&] {
-        check_tiled(e, cfg);
-        if (tile_begin < 0 || tile_begin >= e->k || tile_begin % cfg->tile_size)
-            throw std::invalid_argument("plnmf_gpu_w_phase3: not a tile start");
-        const int64_t en = std::min(e->k, tile_begin + cfg->tile_size);
-        e->launches += kern::shard_phase3(e->s, e->math, e->v, e->k, tile_begin, en, e->w_new, e->q);
-    });
-}
-
-plnmf_status plnmf_gpu_w_end(plnmf_gpu_engine* e) {
-    return guarded([&] {
-        check_engine(e);
-        std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
-        e->s_valid = false;
-    e->r_valid = false;
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-    });
-}
-
-plnmf_status plnmf_gpu_local_pw(plnmf_gpu_engine* e, double* out) {
-    return guarded([&] {
-        check_engine(e);
-        if (!out) throw std::invalid_argument("plnmf_gpu_local_pw: null output");
-        e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
-        PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars, e->scalars, sizeof(double), cudaMemcpyDeviceToHost, e->s));
-        PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
-        *out = e->host_scalars[0];
-    });
-}
-
 // One FAST-HALS iteration in the reference's order (solver.cpp:79-92).  (A
 // CUDA-graph replay of whole iterations was measured slower, 1.73 vs 1.65 ms,
 // and removed: the GPU is never idle between these launches.)
@@ -1258,6 +1101,7 @@ plnmf_status plnmf_gpu_run_iterations(plnmf_gpu_engine* e, const plnmf_config* c
         }
         PLNMF_CUDA_CHECK(cudaEventRecord(b, e->s));
         PLNMF_CUDA_CHECK(cudaEventSynchronize(b));
+        if (e->shard) plnmf::shard::check_error(e);
         if (device_ms) *device_ms = elapsed_s(a, b) * 1e3;
         double ph[4] = {0, 0, 0, 0};
         for (int64_t i = 0; i < n; ++i) {
@@ -1280,6 +1124,7 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
     return guarded([&] {
         check_engine(e);
         if (!cfg || reps < 1) throw std::invalid_argument("plnmf_gpu_time_kernel: bad argument");
+        if (e->shard) throw std::invalid_argument("plnmf_gpu_time_kernel: not available on a shard engine");
         cudaEvent_t a = event_at(e, 0), b = event_at(e, 1);
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
@@ -1432,6 +1277,7 @@ plnmf_status plnmf_gpu_synchronize(plnmf_gpu_engine* e) {
         check_engine(e);
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
         PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s2));
+        if (e->shard) plnmf::shard::check_error(e);
     });
 }
 

@@ -37,11 +37,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Called by one full warp; returns sqrt(sum) in every lane.  trace (debug,
+// Called by one full warp; returns the grid's sum in every lane.  trace (debug,
 // PLNMF_TRACE_EXCHANGE): per column and CTA the SM clock at arrival, at
 // counter completion, and after the partials are read.
-__device__ __forceinline__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
-                                                unsigned long long* trace = nullptr) {
+__device__ __forceinline__ double grid_exchange_sum(double blk, int t, int g, double* partials, unsigned* counters,
+                                                    unsigned long long* trace = nullptr) {
     static_assert(kMaxPartialsPerLane == 8, "tree8 sums the partials of one lane");
     const int lane = lane_id();
     const int64_t stride = partial_stride(g);
@@ -78,7 +78,13 @@ __device__ __forceinline__ double grid_exchange(double blk, int t, int g, double
     }
     const double s = warp_sum_all(tree8(v));
     if (tr && lane == 0) tr[2] = clock64();
-    return __dsqrt_rn(s);
+    return s;
+}
+
+// sqrt of the grid's sum (the column norm, tiled.cpp:137).
+__device__ __forceinline__ double grid_exchange(double blk, int t, int g, double* partials, unsigned* counters,
+                                                unsigned long long* trace = nullptr) {
+    return __dsqrt_rn(grid_exchange_sum(blk, t, g, partials, counters, trace));
 }
 
 

@@ -28,13 +28,13 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
     return z ^ (z >> 31);
 }
 
-// Walks row r's cells; FILL: writes (col, value) from out offset `at`.
-template <bool FILL>
-__device__ int64_t synth_row(int64_t r, int64_t cols, bool dense, double inv_log_q, uint64_t seed, int32_t* ci,
-                             double* val) {
+// Walks row r's cells in ascending column order, calling f(col, value) for
+// each; f returns false to stop the walk early.
+template <class F>
+__device__ void synth_walk(int64_t r, int64_t cols, bool dense, double inv_log_q, uint64_t seed, F&& f) {
     uint64_t s = seed ^ (0xD1B54A32D192ED03ULL * (static_cast<uint64_t>(r) + 1));
     splitmix64(s);
-    int64_t c = -1, n = 0;
+    int64_t c = -1;
     for (;;) {
         int64_t gap = 0;
         if (!dense) {
@@ -47,25 +47,89 @@ __device__ int64_t synth_row(int64_t r, int64_t cols, bool dense, double inv_log
         if (c >= cols) break;
         const double u = static_cast<double>(splitmix64(s) >> 11) * 0x1.0p-53;
         const float value = static_cast<float>(dadd(0.1, dmul(1.9, u)));
-        if (FILL) {
-            ci[n] = static_cast<int32_t>(c);
-            val[n] = static_cast<double>(value);
-        }
-        ++n;
+        if (!f(c, value)) break;
     }
-    return n;
 }
 
-__global__ void synth_count_kernel(int64_t rows, int64_t cols, int dense, double inv_log_q, uint64_t seed,
-                                   int64_t* counts) {
+__global__ void synth_count_kernel(int64_t rows, int64_t row0, int64_t cols, int dense, double inv_log_q,
+                                   uint64_t seed, int64_t* counts) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < rows) counts[r] = synth_row<false>(r, cols, dense, inv_log_q, seed, nullptr, nullptr);
+    if (r >= rows) return;
+    int64_t n = 0;
+    synth_walk(row0 + r, cols, dense, inv_log_q, seed, [&](int64_t, float) { ++n; return true; });
+    counts[r] = n;
 }
 
-__global__ void synth_fill_kernel(int64_t rows, int64_t cols, int dense, double inv_log_q, uint64_t seed,
-                                  const int64_t* __restrict__ rp, int32_t* ci, double* val) {
+__global__ void synth_fill_kernel(int64_t rows, int64_t row0, int64_t cols, int dense, double inv_log_q,
+                                  uint64_t seed, const int64_t* __restrict__ rp, int32_t* ci, double* val) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < rows) synth_row<true>(r, cols, dense, inv_log_q, seed, ci + rp[r], val + rp[r]);
+    if (r >= rows) return;
+    int64_t at = rp[r];
+    synth_walk(row0 + r, cols, dense, inv_log_q, seed, [&](int64_t c, float v) {
+        ci[at] = static_cast<int32_t>(c);
+        val[at] = static_cast<double>(v);
+        ++at;
+        return true;
+    });
+}
+
+// the entries of every row with column in [c_lo, c_hi): count, then fill as
+// (column - c_lo, source row, value) in row-major order
+__global__ void synth_block_count_kernel(int64_t rows, int64_t cols, int dense, double inv_log_q, uint64_t seed,
+                                         int64_t c_lo, int64_t c_hi, int64_t* counts) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int64_t n = 0;
+    synth_walk(r, cols, dense, inv_log_q, seed, [&](int64_t c, float) {
+        if (c >= c_hi) return false;
+        if (c >= c_lo) ++n;
+        return true;
+    });
+    counts[r] = n;
+}
+
+__global__ void synth_block_fill_kernel(int64_t rows, int64_t cols, int dense, double inv_log_q, uint64_t seed,
+                                        int64_t c_lo, int64_t c_hi, const int64_t* __restrict__ offs, int32_t* key,
+                                        int32_t* src, double* val) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int64_t at = offs[r];
+    synth_walk(r, cols, dense, inv_log_q, seed, [&](int64_t c, float v) {
+        if (c >= c_hi) return false;
+        if (c >= c_lo) {
+            key[at] = static_cast<int32_t>(c - c_lo);
+            src[at] = static_cast<int32_t>(r);
+            val[at] = static_cast<double>(v);
+            ++at;
+        }
+        return true;
+    });
+}
+
+__global__ void gather_block_kernel(int64_t m, const int32_t* __restrict__ perm, const int32_t* __restrict__ src,
+                                    const double* __restrict__ v, int32_t* ci, double* val) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = perm[i];
+        ci[i] = src[j];
+        val[i] = v[j];
+    }
+}
+
+// rp[r] = first entry whose (sorted) key is >= r
+__global__ void key_row_ptr_kernel(int64_t rows, int64_t m, const int32_t* __restrict__ keys, int64_t* rp) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows) return;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    rp[r] = lo;
+}
+
+__global__ void iota_kernel(int64_t m, int32_t* x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = (int32_t)i;
 }
 
 __global__ void coo_keys_kernel(int64_t n, int64_t cols, const int64_t* __restrict__ r, const int64_t* __restrict__ c,
@@ -116,7 +180,7 @@ inline unsigned blocks(int64_t n, int t) { return (unsigned)std::max<int64_t>(1,
 namespace kern {
 
 int64_t synth_csr_device(cudaStream_t s, int64_t rows, int64_t cols, double density, uint64_t seed,
-                         int64_t** rp_out, int32_t** ci_out, double** val_out) {
+                         int64_t** rp_out, int32_t** ci_out, double** val_out, int64_t row0) {
     if (rows < 0 || cols < 0) throw std::invalid_argument("synth_csr: negative dimension");
     if (!(density >= 0.0) || density > 1.0) throw std::invalid_argument("synth_csr: density must be in [0, 1]");
     if (cols > INT32_MAX) throw std::invalid_argument("synth_csr: columns exceed int32 indexing");
@@ -126,7 +190,7 @@ int64_t synth_csr_device(cudaStream_t s, int64_t rows, int64_t cols, double dens
     PLNMF_CUDA_CHECK(cudaMalloc(&rp, sizeof(int64_t) * (rows + 1)));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(rp, 0, sizeof(int64_t) * (rows + 1), s));
     if (density > 0.0 && rows > 0) {
-        synth_count_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, cols, dense, inv_log_q, seed, rp + 1);
+        synth_count_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, row0, cols, dense, inv_log_q, seed, rp + 1);
         PLNMF_CUDA_CHECK(cudaGetLastError());
         size_t tmp_bytes = 0;
         PLNMF_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, rp + 1, rp + 1, rows, s));
@@ -143,13 +207,84 @@ int64_t synth_csr_device(cudaStream_t s, int64_t rows, int64_t cols, double dens
     PLNMF_CUDA_CHECK(cudaMalloc(&ci, sizeof(int32_t) * std::max<int64_t>(1, nnz)));
     PLNMF_CUDA_CHECK(cudaMalloc(&val, sizeof(double) * std::max<int64_t>(1, nnz)));
     if (nnz > 0) {
-        synth_fill_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, cols, dense, inv_log_q, seed, rp, ci, val);
+        synth_fill_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, row0, cols, dense, inv_log_q, seed, rp, ci, val);
         PLNMF_CUDA_CHECK(cudaGetLastError());
     }
     *rp_out = rp;
     *ci_out = ci;
     *val_out = val;
     return nnz;
+}
+
+int64_t synth_transpose_block_device(cudaStream_t s, int64_t rows, int64_t cols, double density, uint64_t seed,
+                                     int64_t c_lo, int64_t c_hi, int64_t** rp_out, int32_t** ci_out,
+                                     double** val_out) {
+    if (rows < 0 || cols < 0 || c_lo < 0 || c_hi < c_lo || c_hi > cols)
+        throw std::invalid_argument("synth_csr: bad column block");
+    if (!(density >= 0.0) || density > 1.0) throw std::invalid_argument("synth_csr: density must be in [0, 1]");
+    if (rows > INT32_MAX || cols > INT32_MAX) throw std::invalid_argument("synth_csr: dimensions exceed int32 indexing");
+    const bool dense = density >= 1.0;
+    const double inv_log_q = (dense || density <= 0.0) ? 0.0 : 1.0 / std::log1p(-density);  // host, as host.cpp
+    const int64_t nb = c_hi - c_lo;
+    int64_t* rp = nullptr;
+    PLNMF_CUDA_CHECK(cudaMalloc(&rp, sizeof(int64_t) * (nb + 1)));
+    int64_t m = 0;
+    int64_t* offs = nullptr;
+    PLNMF_CUDA_CHECK(cudaMallocAsync(&offs, sizeof(int64_t) * (rows + 1), s));
+    PLNMF_CUDA_CHECK(cudaMemsetAsync(offs, 0, sizeof(int64_t) * (rows + 1), s));
+    if (density > 0.0 && rows > 0 && nb > 0) {
+        synth_block_count_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, cols, dense, inv_log_q, seed, c_lo, c_hi,
+                                                                   offs + 1);
+        PLNMF_CUDA_CHECK(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        PLNMF_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, offs + 1, offs + 1, rows, s));
+        void* tmp = nullptr;
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&tmp, tmp_bytes, s));
+        PLNMF_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, offs + 1, offs + 1, rows, s));
+        PLNMF_CUDA_CHECK(cudaFreeAsync(tmp, s));
+        PLNMF_CUDA_CHECK(cudaMemcpyAsync(&m, offs + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    if (m > INT32_MAX) throw std::invalid_argument("synth_csr: column block exceeds int32 entries");
+    int32_t* ci = nullptr;
+    double* val = nullptr;
+    PLNMF_CUDA_CHECK(cudaMalloc(&ci, sizeof(int32_t) * std::max<int64_t>(1, m)));
+    PLNMF_CUDA_CHECK(cudaMalloc(&val, sizeof(double) * std::max<int64_t>(1, m)));
+    if (m == 0) {
+        PLNMF_CUDA_CHECK(cudaMemsetAsync(rp, 0, sizeof(int64_t) * (nb + 1), s));
+    } else {
+        int32_t *key, *key_sorted, *src, *idx, *perm;
+        double* v;
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&key, sizeof(int32_t) * m, s));
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&key_sorted, sizeof(int32_t) * m, s));
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&src, sizeof(int32_t) * m, s));
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&idx, sizeof(int32_t) * m, s));
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&perm, sizeof(int32_t) * m, s));
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&v, sizeof(double) * m, s));
+        synth_block_fill_kernel<<<blocks(rows, 128), 128, 0, s>>>(rows, cols, dense, inv_log_q, seed, c_lo, c_hi, offs,
+                                                                  key, src, v);
+        iota_kernel<<<blocks(m, 256) < 4736 ? blocks(m, 256) : 4736, 256, 0, s>>>(m, idx);
+        int bits = 1;
+        while (bits < 31 && (int64_t(1) << bits) < nb) ++bits;
+        size_t tmp_bytes = 0;
+        const int mi = (int)m;
+        // stable: equal columns keep ascending source rows (the transpose order)
+        PLNMF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_sorted, idx, perm, mi, 0, bits, s));
+        void* tmp = nullptr;
+        PLNMF_CUDA_CHECK(cudaMallocAsync(&tmp, tmp_bytes, s));
+        PLNMF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_sorted, idx, perm, mi, 0, bits, s));
+        gather_block_kernel<<<blocks(m, 256) < 4736 ? blocks(m, 256) : 4736, 256, 0, s>>>(m, perm, src, v, ci, val);
+        key_row_ptr_kernel<<<blocks(nb + 1, 256), 256, 0, s>>>(nb, m, key_sorted, rp);
+        PLNMF_CUDA_CHECK(cudaGetLastError());
+        for (void* p : {(void*)key, (void*)key_sorted, (void*)src, (void*)idx, (void*)perm, (void*)v, tmp})
+            PLNMF_CUDA_CHECK(cudaFreeAsync(p, s));
+    }
+    PLNMF_CUDA_CHECK(cudaFreeAsync(offs, s));
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(s));
+    *rp_out = rp;
+    *ci_out = ci;
+    *val_out = val;
+    return m;
 }
 
 int64_t coo_to_csr_device(cudaStream_t s, int64_t rows, int64_t cols, int64_t n, const int64_t* r_host,

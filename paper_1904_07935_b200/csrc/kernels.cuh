@@ -10,6 +10,7 @@
 #include <string>
 
 #include "host.hpp"
+#include "peer.cuh"
 
 namespace plnmf {
 
@@ -88,9 +89,12 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
                              bool force_streaming = false);
 // Streaming fallback (stream.cu): phase A + one persistent streaming launch.
 PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize, int device);
+// xch (sharded W update, world > 1): every column's sum of squares is also
+// exchanged with the other ranks over peer memory (peer.cuh: world_sum).
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
-                  const double* add, double* norms, double* partials, unsigned* counters);
+                  const double* add, double* norms, double* partials, unsigned* counters,
+                  const WorldXch* xch = nullptr);
 // init_new_accumulator + phase1_left_contributions into nb (tiled.cpp:28-65).
 int stream_phase_a(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
                    const double* coeff, double* nb);
@@ -146,12 +150,47 @@ int64_t direct_residual_partials(int64_t v, int64_t d);
 // ---- input construction on the device (ingest.cu) ---------------------------------
 // The synthetic CSR of plnmf_synth_csr generated on the device; returns nnz and
 // cudaMalloc'ed arrays (the caller owns them).
+// row0: global index of the first generated row (a shard's row block).
 int64_t synth_csr_device(cudaStream_t s, int64_t rows, int64_t cols, double density, uint64_t seed,
-                         int64_t** rp, int32_t** ci, double** val);
+                         int64_t** rp, int32_t** ci, double** val, int64_t row0 = 0);
+// CSR of the transpose's row block [c_lo, c_hi) of the synthetic rows x cols
+// matrix (the shard's column block of A): rows of the output are columns of A,
+// entries in ascending source-row order (transpose() order,
+// proj/src/csr_matrix.cpp:30-50), column indices = global source rows.
+int64_t synth_transpose_block_device(cudaStream_t s, int64_t rows, int64_t cols, double density, uint64_t seed,
+                                     int64_t c_lo, int64_t c_hi, int64_t** rp, int32_t** ci, double** val);
 // read_coordinate's assembly (matrix_market.cpp:147-172) of n host COO entries
 // (0-based, file order); returns nnz and cudaMalloc'ed CSR arrays.
 int64_t coo_to_csr_device(cudaStream_t s, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
                           const int64_t* c, const double* v, int64_t** rp, int32_t** ci, double** val);
+
+// ---- sharded engine: peer-memory collectives (peer.cu) -----------------------------
+// Byte offsets of the sections of one rank's window (identical on every rank).
+struct PeerLayout {
+    int world = 1;
+    int64_t vcap = 0, dcap = 0, k = 0;
+    size_t off_wfull[2] = {0, 0}, off_hfull[2] = {0, 0};  // double-buffered full factors, world * cap rows
+    size_t off_sparts = 0, off_qparts = 0;                // world K x K Gram partials (slot = source rank)
+    size_t off_pw = 0;                                    // kMaxWorld scalar partials
+    size_t off_xvals = 0, off_xflags = 0;                 // norm exchange slots, xch_slot(t, rep, src)
+    size_t off_agflags = 0;                               // all-gather flags [channel][source rank]
+    size_t off_error = 0;                                 // timeout word
+    size_t total = 0;
+};
+PeerLayout peer_layout(int world, int64_t vcap, int64_t dcap, int64_t k);
+// Store `bytes` of src into dst.p[p] for every rank p (except this rank when
+// skip_self), then release flag.p[p] = epoch in every window.  done: a zeroed
+// local counter.
+int peer_push(cudaStream_t s, const void* src, int64_t bytes, const PeerPtrs& dst, int world, int rank,
+              bool skip_self, const PeerPtrs& flag, unsigned epoch, unsigned* done, int sms);
+// Block the stream until flags[0..world) == epoch (bounded: sets *error on timeout).
+int peer_wait(cudaStream_t s, const unsigned* flags, int world, unsigned epoch, int* error,
+              unsigned long long timeout_ns);
+// out[i] := parts[0*stride + i] + parts[1*stride + i] + ... in rank order.
+int sum_parts(cudaStream_t s, const double* parts, int world, int64_t n, int64_t stride, double* out);
+// Global indices of a balanced contiguous split of n over world ranks -> padded
+// positions owner * cap + (x - lo(owner)).
+int remap_split_index(cudaStream_t s, int32_t* idx, int64_t nnz, int64_t n, int world, int64_t cap);
 
 // ---- layout / structure ------------------------------------------------------------
 // dst (rows x cols, row-major) := src (rows x cols, column-major), and back.

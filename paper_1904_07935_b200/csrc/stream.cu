@@ -104,9 +104,12 @@ struct StreamArgs {
     double* norms;
     double* partials;
     unsigned* counters;
+    WorldXch xch;  // WORLD: the other ranks' windows (sharded engine)
 };
 
-template <class M, bool NORMALIZE>
+// WORLD: the sharded W update — the column's sum is the rank-local grid sum
+// followed by the cross-rank exchange over peer memory (peer.cuh: world_sum).
+template <class M, bool NORMALIZE, bool WORLD = false>
 __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs p) {
     __shared__ double red[48];
     const int k = p.k, T = p.tile, tid = threadIdx.x;
@@ -144,7 +147,10 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs 
             if (NORMALIZE) {
                 const double blk = block_sum(ss, red);
                 if (tid < kWarp) {
-                    const double nrm = grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
+                    const double nrm =
+                        WORLD ? __dsqrt_rn(world_sum(grid_exchange_sum(blk, t, gridDim.x, p.partials, p.counters), t,
+                                                     p.xch))
+                              : grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
                     if (tid == 0) {
                         red[40] = nrm;
                         if (blockIdx.x == 0) p.norms[t] = nrm;
@@ -234,7 +240,7 @@ PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize
 
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
-                  const double* add, double* norms, double* partials, unsigned* counters) {
+                  const double* add, double* norms, double* partials, unsigned* counters, const WorldXch* xch) {
     if (n <= 0 || k <= 0) return 0;
     // phase A: init + phase 1 into `out` (used as the accumulator nb)
     const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
@@ -243,14 +249,23 @@ int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int
     else
         stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
     PLNMF_CUDA_CHECK(cudaGetLastError());
-    StreamArgs a{n, (int)k, (int)tile, eps, plan.rows_per_cta, old_m, out, coeff, add, norms, partials, counters};
+    const bool world = xch && xch->world > 1;
+    StreamArgs a{n, (int)k, (int)tile, eps, plan.rows_per_cta, old_m, out, coeff, add, norms, partials, counters,
+                 world ? *xch : WorldXch{}};
     const dim3 grid((unsigned)plan.grid), block(kSThreads);
     if (w_update) {
         exchange_reset(s, k, plan.grid, partials, counters);
         void* args[] = {&a};
-        const void* fn = (m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
-                                            : (const void*)stream_update_kernel<MathFused, true>;
-        PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+        const void* fn = world ? ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true, true>
+                                                     : (const void*)stream_update_kernel<MathFused, true, true>)
+                               : ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
+                                                     : (const void*)stream_update_kernel<MathFused, true>);
+        // a plan with fewer CTAs than SMs (ranks sharing one GPU) is co-resident with
+        // the other ranks' kernels only under a plain launch
+        if (plan.cooperative)
+            PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+        else
+            PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, 0, s));
     } else if (m == Math::exact) {
         stream_update_kernel<MathExact, false><<<grid, block, 0, s>>>(a);
     } else {

@@ -1,154 +1,24 @@
-"""The multi-GPU (sharded) iteration driver, exercised on CPU with gloo and
-world_size 2.  The driver (paper_1904_07935_b200.sharded) is
-the product code; the compute backend here is a numpy restatement of the
-engine's shard-mode steps (test infrastructure), so the test checks the
-partitioning, the rank-ordered collectives and the column-stepped W update:
-a 2-rank run must equal a 1-rank run to ~1 ulp and match the oracle."""
+"""The sharded engine's host side on CPU: the row/column
+partition, the shard blocks, and the rank bootstrap of
+paper_1904_07935_b200.sharded.connect over torch.distributed (gloo,
+world_size 2) — the IPC handles all-gathered in rank order and ||A||^2 chained
+over the ranks, which must equal the reference's single serial sum bit for bit
+(proj/src/input_matrix.cpp:15-20).  The device side runs in
+test_sharded_gpu.py.  Plus the arithmetic the sharded iteration promises: with
+the K x K Gram partials and the norm partials summed in rank order, one
+iteration stays within ~1 ulp of the unsharded reference iteration."""
 import os
 import socket
 
 import numpy as np
-import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from _helpers import Restated as R, rel_max
 from paper_1904_07935_b200 import plnmf as P
-from paper_1904_07935_b200.sharded import ShardedNMF, ShardPlan, shard_blocks
+from paper_1904_07935_b200.sharded import ShardPlan, connect, shard_blocks
 
-
-def clamp(eps, x):
-    return np.where(eps < x, x, eps)
-
-
-class NumpyShardBackend:
-    """Shard-mode engine semantics on CPU tensors (row-major buffers)."""
-
-    def __init__(self, plan, rank, rows, cols, k, w0, ht0):
-        self.torch = torch
-        self.plan, self.rank, self.k = plan, rank, k
-        self.rows, self.cols = rows, cols
-        self.v_lo, self.v_hi = plan.v_range(rank)
-        self.d_lo, self.d_hi = plan.d_range(rank)
-        self.W = torch.tensor(np.ascontiguousarray(w0[self.v_lo:self.v_hi]))
-        self.Ht = torch.tensor(np.ascontiguousarray(ht0[self.d_lo:self.d_hi]))
-        self.W_full = torch.zeros((plan.v, k), dtype=torch.float64)
-        self.Ht_full = torch.zeros((plan.d, k), dtype=torch.float64)
-        self.S = torch.zeros((k, k), dtype=torch.float64)
-        self.Q = torch.zeros((k, k), dtype=torch.float64)
-        self.col_ss = torch.zeros(1, dtype=torch.float64)
-        self.world_ss = torch.zeros(plan.world, dtype=torch.float64)
-        self.P = self.R = None
-
-    def sync(self):
-        pass
-
-    def publish(self):
-        self.W_full[self.v_lo:self.v_hi] = self.W
-        self.Ht_full[self.d_lo:self.d_hi] = self.Ht
-
-    def products_h(self):
-        c = self.cols
-        self.R = R.spmm(c.rows, c.cols, c.row_ptr, c.col_idx, c.values, self.W_full.numpy())
-        self.S.copy_(torch.tensor(R.gram(self.W.numpy())))
-
-    def products_w(self):
-        r = self.rows
-        self.P = R.spmm(r.rows, r.cols, r.row_ptr, r.col_idx, r.values, self.Ht_full.numpy())
-        self.Q.copy_(torch.tensor(R.gram(self.Ht.numpy())))
-
-    def update_h(self, cfg, algorithm):
-        ht, _ = R.update_tiled(self.Ht.numpy(), self.S.numpy(), self.R, cfg.tile_size, cfg.epsilon, is_w=False)
-        self.Ht = torch.tensor(np.ascontiguousarray(ht))
-
-    def w_begin(self, cfg):
-        w, q, k, T = self.W.numpy(), self.Q.numpy(), self.k, cfg.tile_size
-        nb = w * np.diag(q)[None, :]  # tiled.cpp:44
-        for tau in range(1, (k + T - 1) // T):
-            b, e = tau * T, min(k, tau * T + T)
-            for j in range(b):
-                for kk in range(b, e):
-                    nb[:, j] = nb[:, j] + (-1.0 * q[kk, j]) * w[:, kk]
-        self.nb = nb
-
-    def w_column_step(self, cfg, t):
-        T, w, q, nb = cfg.tile_size, self.W.numpy(), self.Q.numpy(), self.nb
-        b, e = (t // T) * T, min(self.k, (t // T) * T + T)
-        s = np.zeros(nb.shape[0])
-        for kk in range(b, t):
-            s = s + nb[:, kk] * q[kk, t]
-        for kk in range(t, e):
-            s = s + w[:, kk] * q[kk, t]
-        nb[:, t] = clamp(cfg.epsilon, (nb[:, t] + self.P[:, t]) - s)
-        self.col_ss[0] = float((nb[:, t] * nb[:, t]).sum())
-
-    def w_normalize(self, cfg, t):
-        tot = 0.0
-        for x in self.world_ss.tolist():
-            tot = tot + x
-        self.nb[:, t] = clamp(cfg.epsilon, self.nb[:, t] / np.sqrt(tot))
-
-    def w_phase3(self, cfg, b):
-        T, q, nb = cfg.tile_size, self.Q.numpy(), self.nb
-        e = min(self.k, b + T)
-        for c in range(e, self.k):
-            for kk in range(b, e):
-                nb[:, c] = nb[:, c] + (-1.0 * q[kk, c]) * nb[:, kk]
-
-    def w_end(self):
-        self.W = torch.tensor(np.ascontiguousarray(self.nb))
-
-    def local_pw(self):
-        return float((self.P * self.W.numpy()).sum())
-
-
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
-K, TILE, V, D = 7, 3, 60, 45
-
-
-def conditioned_state():
-    """The oracle's fast-hals state after 6 iterations from the seed: past the
-    collapse of iteration 1, where ~1-ulp differences stay ~1 ulp."""
-    m = P.synth_csr(V, D, 0.15, 5)
-    w, ht = R.init_factors(V, D, K, seed=2)
-    trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
-    for _ in range(6):
-        ht = R.update_h_reference(ht, R.spmm(D, V, trp, tci, tval, w), R.gram(w))
-        w, _ = R.update_w_reference(w, R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht), R.gram(ht))
-    return m, w, ht
-
-
-def _worker(rank, world, port, out_dir):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        k, tile = K, TILE
-        m, w_s, ht_s = conditioned_state()
-        w0, ht0 = np.ascontiguousarray(w_s), np.ascontiguousarray(ht_s)
-        plan = ShardPlan(V, D, world)
-        rows, cols = shard_blocks(m, plan, rank)
-        backend = NumpyShardBackend(plan, rank, rows, cols, k, w0, ht0)
-        drv = ShardedNMF(backend, plan, rank, R.norm_sq(m.values))
-        tr = drv.iterate(P.SolverConfig(rank=k, tile_size=tile, max_iters=3, rel_tol=0.0), P.Algorithm.tiled)
-        np.savez(os.path.join(out_dir, f"w{world}_r{rank}.npz"), w=backend.W.numpy(), ht=backend.Ht.numpy(),
-                 init=tr.initial_error, rel=np.array(tr.rel_errors))
-    finally:
-        dist.destroy_process_group()
-
-
-def _run(world, tmp_path):
-    port = _free_port()
-    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
-    parts = [np.load(tmp_path / f"w{world}_r{g}.npz") for g in range(world)]
-    w = np.concatenate([p["w"] for p in parts])
-    ht = np.concatenate([p["ht"] for p in parts])
-    return w, ht, parts
+V, D, K, TILE = 60, 45, 7, 3
 
 
 def test_shard_plan_covers_rows_and_blocks_are_exact():
@@ -169,20 +39,118 @@ def test_shard_plan_covers_rows_and_blocks_are_exact():
         assert np.array_equal(cols.col_idx, tci[e0:e1]) and np.array_equal(cols.values, tval[e0:e1])
 
 
-def test_two_ranks_gloo_match_one_rank_and_the_oracle(tmp_path):
-    w2, ht2, p2 = _run(2, tmp_path)
-    w1, ht1, p1 = _run(1, tmp_path)
-    # the 2-rank run differs from the 1-rank run only in Gram / norm partial order
-    assert rel_max(w1, w2) <= 1e-12 and rel_max(ht1, ht2) <= 1e-12
-    assert abs(float(p2[0]["init"]) - float(p1[0]["init"])) <= 1e-14 * float(p1[0]["init"])
-    assert np.allclose(p2[0]["rel"], p1[0]["rel"], rtol=1e-10, atol=0)
-    assert np.array_equal(p2[0]["rel"], p2[1]["rel"])  # every rank reports the same objective
-    # one rank = the reference's tiled iteration (restatement), to ~1 ulp
+class HostShard:
+    """The bootstrap surface of ShardEngine (ipc_handle, connect_handles,
+    norm_sq_from, set_norm_sq) over a host row block: what connect() drives."""
+
+    def __init__(self, m, world, rank):
+        self.world, self.shard_rank = world, rank
+        self.rows, _ = shard_blocks(m, ShardPlan(m.rows, m.cols, world), rank)
+        self.handles = None
+        self.norm_sq = None
+
+    def ipc_handle(self):
+        return bytes([self.shard_rank + 1]) * 64
+
+    def connect_handles(self, handles):
+        self.handles = list(handles)
+
+    def norm_sq_from(self, start):
+        acc = start
+        for x in self.rows.values.tolist():
+            acc += x * x
+        return acc
+
+    def set_norm_sq(self, value):
+        self.norm_sq = value
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _bootstrap_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = P.synth_csr(V, D, 0.15, 5)
+        eng = HostShard(m, world, rank)
+        connect(eng)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), handles=np.frombuffer(b"".join(eng.handles), np.uint8),
+                 norm=eng.norm_sq)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_connect_gathers_handles_and_chains_the_norm_over_gloo(tmp_path):
+    world = 2
+    mp.spawn(_bootstrap_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    m = P.synth_csr(V, D, 0.15, 5)
+    want = b"".join(bytes([g + 1]) * 64 for g in range(world))
+    for g in range(world):
+        out = np.load(tmp_path / f"r{g}.npz")
+        assert out["handles"].tobytes() == want  # rank order
+        assert float(out["norm"]) == R.norm_sq(m.values)  # the single serial sum, bit for bit
+
+
+def conditioned_state():
+    m = P.synth_csr(V, D, 0.15, 5)
+    w, ht = R.init_factors(V, D, K, seed=2)
+    trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
+    for _ in range(6):
+        ht = R.update_h_reference(ht, R.spmm(D, V, trp, tci, tval, w), R.gram(w))
+        w, _ = R.update_w_reference(w, R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht), R.gram(ht))
+    return m, w, ht
+
+
+def sharded_iteration(m, w, ht, world):
+    """One tiled iteration with the sharded engine's summation structure: the
+    Gram products as rank-ordered sums of the ranks' partials, each W column
+    norm as the rank-ordered sum of the ranks' sums of squares
+    (csrc/shard_engine.cu, peer.cuh: world_sum); everything else is the
+    reference's per-element order."""
+    plan = ShardPlan(V, D, world)
+    vr = [plan.v_range(g) for g in range(world)]
+    dr = [plan.d_range(g) for g in range(world)]
+    trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
+    s = sum(R.gram(np.ascontiguousarray(w[slice(*x)])) for x in vr)
+    ht, _ = R.update_tiled(ht, s, R.spmm(D, V, trp, tci, tval, w), TILE, is_w=False)
+    q = sum(R.gram(np.ascontiguousarray(ht[slice(*x)])) for x in dr)
+    p = R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht)
+    # the W update with the norm partials per rank: phase 2 column by column
+    nb = w * np.diag(q)[None, :]
+    for tau in range(1, (K + TILE - 1) // TILE):
+        b, e = tau * TILE, min(K, tau * TILE + TILE)
+        for j in range(b):
+            for kk in range(b, e):
+                nb[:, j] = nb[:, j] + (-1.0 * q[kk, j]) * w[:, kk]
+    for b in range(0, K, TILE):
+        e = min(K, b + TILE)
+        for t in range(b, e):
+            acc = np.zeros(V)
+            for kk in range(b, t):
+                acc = acc + nb[:, kk] * q[kk, t]
+            for kk in range(t, e):
+                acc = acc + w[:, kk] * q[kk, t]
+            nb[:, t] = np.maximum(1e-16, (nb[:, t] + p[:, t]) - acc)
+            tot = 0.0
+            for x in vr:
+                tot += float(np.sum(nb[slice(*x), t] ** 2))
+            nb[:, t] = np.maximum(1e-16, nb[:, t] / np.sqrt(tot))
+        for c in range(e, K):
+            for kk in range(b, e):
+                nb[:, c] = nb[:, c] + (-1.0 * q[kk, c]) * nb[:, kk]
+    return nb, ht
+
+
+def test_sharded_summation_stays_within_an_ulp_of_the_reference_iteration():
     m, w, ht = conditioned_state()
     trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
-    for _ in range(3):
-        r = R.spmm(D, V, trp, tci, tval, w)
-        ht, _ = R.update_tiled(ht, R.gram(w), r, TILE, is_w=False)
-        p = R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht)
-        w, _ = R.update_tiled(w, R.gram(ht), p, TILE, is_w=True)
-    assert rel_max(w, w1) <= 1e-10 and rel_max(ht, ht1) <= 1e-10
+    ht_ref, _ = R.update_tiled(ht, R.gram(w), R.spmm(D, V, trp, tci, tval, w), TILE, is_w=False)
+    w_ref, _ = R.update_tiled(w, R.gram(ht_ref), R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht_ref), TILE,
+                              is_w=True)
+    for world in (1, 2, 3):
+        w_sh, ht_sh = sharded_iteration(m, w, ht, world)
+        assert rel_max(ht_ref, ht_sh) <= 1e-13 and rel_max(w_ref, w_sh) <= 1e-12

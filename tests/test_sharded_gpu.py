@@ -1,84 +1,227 @@
-"""The sharded engine's device kernels (plnmf_gpu_create_shard, the products
-on gathered factors, the column-stepped W update) through the real driver.
-Only one GPU is available here, so the ranks share cuda:0 over gloo (NCCL
-refuses two ranks on one device); the multi-GPU launch differs only in the
-process-group backend."""
+"""The sharded engine (csrc/shard_engine.cu) on the device: several ranks in
+one process share cuda:0 (plnmf_gpu_shard_connect_local gives each rank's
+persistent W kernel an equal share of the SMs), each driven from its own host
+thread, exactly as one process per GPU would drive them.  The ranks exchange
+everything through their peer windows — the factor / Gram all-gathers and the
+per-column W norm inside the persistent kernel — so these tests run the same
+device code as the multi-GPU launch; only the window mapping differs (the same
+device's pointers instead of CUDA IPC over NVLink).  Ranks that share a GPU
+wait on one another's kernels, which CUDA's lazy module loading can deadlock,
+so every case runs in a fresh process with CUDA_MODULE_LOADING=EAGER.
+
+Checked against the oracle's restatement of the sharded arithmetic (the
+reference's per-element order everywhere; the K x K Gram partials and the
+error partial summed in rank order), bit for bit where the engine promises it
+(R, S, P, Q, Ht), and W to 1e-12 (norm partial order)."""
 import os
-import socket
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
 
 import numpy as np
 import pytest
-import torch
-import torch.distributed as dist
-import torch.multiprocessing as mp
 
-from _helpers import Restated as R, rel_max
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))  # also run as a script (the eager subprocess)
+from _helpers import Restated as R, bits_equal, rel_max
 from paper_1904_07935_b200 import plnmf as P
-from paper_1904_07935_b200.sharded import GpuShardBackend, ShardedNMF, ShardPlan, shard_blocks
+from paper_1904_07935_b200.sharded import ShardEngine, ShardPlan, connect_local
 
 pytestmark = pytest.mark.gpu
 K, TILE, V, D = 24, 5, 1500, 900
 
 
-def conditioned_state():
-    m = P.synth_csr(V, D, 0.02, 9)
-    w, ht = R.init_factors(V, D, K, seed=1)
-    trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
+def conditioned_state(v=V, d=D, k=K, density=0.02, seed=9):
+    """A few fast-hals iterations from the seed: past iteration 1's collapse."""
+    m = P.synth_csr(v, d, density, seed)
+    w, ht = R.init_factors(v, d, k, seed=1)
+    trp, tci, tval = R.transpose(v, d, m.row_ptr, m.col_idx, m.values)
     for _ in range(4):
-        ht = R.update_h_reference(ht, R.spmm(D, V, trp, tci, tval, w), R.gram(w))
-        w, _ = R.update_w_reference(w, R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht), R.gram(ht))
+        ht = R.update_h_reference(ht, R.spmm(d, v, trp, tci, tval, w), R.gram(w))
+        w, _ = R.update_w_reference(w, R.spmm(v, d, m.row_ptr, m.col_idx, m.values, ht), R.gram(ht))
     return m, w, ht
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
+def on_ranks(engines, fn):
+    """fn(engine, g) on every rank concurrently (one host thread per rank)."""
+    with ThreadPoolExecutor(len(engines)) as ex:
+        return list(ex.map(lambda g: fn(engines[g], g), range(len(engines))))
 
 
-def _worker(rank, world, port, out_dir):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        m, w0, ht0 = conditioned_state()
-        plan = ShardPlan(V, D, world)
-        rows, cols = shard_blocks(m, plan, rank)
-        be = GpuShardBackend(0, world, plan, rank, rows, cols, R.norm_sq(m.values), K)
-        (v0, v1), (d0, d1) = plan.v_range(rank), plan.d_range(rank)
-        be.set_local_factors(w0[v0:v1], ht0[d0:d1])
-        drv = ShardedNMF(be, plan, rank, R.norm_sq(m.values))
-        tr = drv.iterate(P.SolverConfig(rank=K, tile_size=TILE, max_iters=2, rel_tol=0.0), P.Algorithm.tiled)
-        w, ht = be.get_local_factors()
-        np.savez(os.path.join(out_dir, f"g{world}_r{rank}.npz"), w=w, ht=ht, init=tr.initial_error,
-                 rel=np.array(tr.rel_errors))
-        be.close()
-    finally:
-        dist.destroy_process_group()
+def make_ranks(m, world, k=K):
+    engines = [ShardEngine.from_csr(m, world, g, k) for g in range(world)]
+    connect_local(engines)
+    return engines
 
 
-def _run(world, tmp_path):
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    parts = [np.load(tmp_path / f"g{world}_r{g}.npz") for g in range(world)]
-    return np.concatenate([p["w"] for p in parts]), np.concatenate([p["ht"] for p in parts]), parts
+def ordered_sum(parts):
+    s = parts[0].copy()
+    for x in parts[1:]:
+        s = s + x
+    return s
 
 
-def test_sharded_engine_matches_single_engine_and_oracle(gpu, tmp_path):
-    w1, ht1, p1 = _run(1, tmp_path)
-    w2, ht2, p2 = _run(2, tmp_path)
-    m, w, ht = conditioned_state()
-    # the unsharded engine on the same state
-    eng = P.Engine(P.InputMatrix(m), K)
-    eng.set_factors(P.FactorPair(w, ht))
-    tr = eng.iterate(P.SolverConfig(rank=K, tile_size=TILE, max_iters=2, rel_tol=0.0), P.Algorithm.tiled)
-    single = eng.get_factors()
-    # the oracle's tiled iterations
+def case_step_products_and_updates(world):
+    m, w0, ht0 = conditioned_state()
+    plan = ShardPlan(V, D, world)
+    vr = [plan.v_range(g) for g in range(world)]
+    dr = [plan.d_range(g) for g in range(world)]
+    engines = make_ranks(m, world)
+    on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*vr[g])], ht0[slice(*dr[g])])))
+    cfg = P.SolverConfig(rank=K, tile_size=TILE)
     trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
-    for _ in range(2):
-        ht, _ = R.update_tiled(ht, R.gram(w), R.spmm(D, V, trp, tci, tval, w), TILE, is_w=False)
-        w, _ = R.update_tiled(w, R.gram(ht), R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht), TILE, is_w=True)
-    for wx, hx in [(w1, ht1), (w2, ht2), (single.w, single.ht)]:
-        assert rel_max(w, wx) <= 1e-10 and rel_max(ht, hx) <= 1e-10
-    assert rel_max(w1, w2) <= 1e-12 and rel_max(ht1, ht2) <= 1e-12
-    assert abs(float(p1[0]["init"]) - tr.initial_error) <= 1e-13 * tr.initial_error
-    assert np.allclose(p1[0]["rel"], [r.rel_error for r in tr.records], rtol=1e-10, atol=0)
-    assert np.array_equal(p2[0]["rel"], p2[1]["rel"])
+
+    # R = A^T W (local rows, bitwise) and S = sum_g gram(W_g) in rank order (bitwise)
+    on_ranks(engines, lambda e, g: e.precompute_h_products())
+    r_full = R.spmm(D, V, trp, tci, tval, w0)
+    s_sh = ordered_sum([R.gram(np.ascontiguousarray(w0[slice(*vr[g])])) for g in range(world)])
+    for g, e in enumerate(engines):
+        assert bits_equal(e.get_product("r"), r_full[slice(*dr[g])])
+        assert bits_equal(e.get_product("s"), s_sh)
+
+    # H update (row-local): bitwise
+    on_ranks(engines, lambda e, g: e.update_h(cfg, P.Algorithm.tiled))
+    ht1, _ = R.update_tiled(ht0, s_sh, r_full, TILE, is_w=False)
+    for g, e in enumerate(engines):
+        assert bits_equal(e.get_factors().ht, ht1[slice(*dr[g])])
+
+    # P = A Ht on the gathered Ht (bitwise), Q in rank order (bitwise)
+    on_ranks(engines, lambda e, g: e.precompute_w_products())
+    p_full = R.spmm(V, D, m.row_ptr, m.col_idx, m.values, ht1)
+    q_sh = ordered_sum([R.gram(np.ascontiguousarray(ht1[slice(*dr[g])])) for g in range(world)])
+    for g, e in enumerate(engines):
+        assert bits_equal(e.get_product("p"), p_full[slice(*vr[g])])
+        assert bits_equal(e.get_product("q"), q_sh)
+
+    # W update: the norm of every column exchanged across the ranks inside the kernel
+    on_ranks(engines, lambda e, g: e.update_w(cfg, P.Algorithm.tiled))
+    w1, norms = R.update_tiled(w0, q_sh, p_full, TILE, is_w=True)
+    w_got = np.concatenate([e.get_factors().w for e in engines])
+    assert rel_max(w1, w_got) <= 1e-12
+    got_norms = [e.get_product("column_norms") for e in engines]
+    assert all(bits_equal(got_norms[0], x) for x in got_norms[1:])  # every rank used the same norms
+    assert np.max(np.abs(got_norms[0] - norms) / norms) <= 1e-13
+
+    # the error: every rank the same bits, the oracle's value to 1e-12
+    reps = on_ranks(engines, lambda e, g: e.evaluate_error())
+    assert all(r.relative == reps[0].relative for r in reps)
+    e_ref = R.relative_error_gram(R.norm_sq(m.values), w1, p_full, q_sh, R.gram(w1))[1]
+    assert abs(reps[0].relative - e_ref) <= 1e-12 * e_ref
+    for e in engines:
+        e.close()
+
+
+def case_iterate_matches_single_engine(world):
+    m, w0, ht0 = conditioned_state()
+    plan = ShardPlan(V, D, world)
+    cfg = P.SolverConfig(rank=K, tile_size=TILE, max_iters=3, rel_tol=0.0)
+    single = P.Engine(P.InputMatrix(m), K)
+    single.set_factors(P.FactorPair(w0, ht0))
+    tr1 = single.iterate(cfg, P.Algorithm.tiled)
+    f1 = single.get_factors()
+
+    engines = make_ranks(m, world)
+    on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*plan.v_range(g))],
+                                                              ht0[slice(*plan.d_range(g))])))
+    trs = on_ranks(engines, lambda e, g: e.iterate(cfg, P.Algorithm.tiled))
+    for tr in trs[1:]:  # every rank reports the same trajectory, bit for bit
+        assert tr.initial_error == trs[0].initial_error
+        assert [r.rel_error for r in tr.records] == [r.rel_error for r in trs[0].records]
+    assert abs(trs[0].initial_error - tr1.initial_error) <= 1e-13 * tr1.initial_error
+    for a, b in zip(trs[0].records, tr1.records):
+        assert abs(a.rel_error - b.rel_error) <= 1e-10 * b.rel_error
+    w = np.concatenate([e.get_factors().w for e in engines])
+    ht = np.concatenate([e.get_factors().ht for e in engines])
+    assert rel_max(f1.w, w) <= 1e-10 and rel_max(f1.ht, ht) <= 1e-10
+    # run_iterations: the same sharded iteration without error evaluation or host syncs
+    ms = on_ranks(engines, lambda e, g: e.run_iterations(cfg, P.Algorithm.tiled, 2))
+    assert all(x > 0 for x in ms)
+    for e in engines:
+        e.close()
+
+
+def case_generated_shards(world):
+    """The C5 path: each rank generates its row block and its A^T block on the
+    device; products from init_factors equal those of shards built from the
+    host generator's CSR, and ||A||^2 chained over the ranks equals the serial sum."""
+    v, d, dens, seed, k = 3000, 2200, 0.01, 20, 16
+    m = P.synth_csr(v, d, dens, seed)
+    gen = [ShardEngine.generate(v, d, dens, seed, k, world, g) for g in range(world)]
+    connect_local(gen, chain_norm=True)
+    host = make_ranks(m, world, k)
+    assert all(e.norm_sq == R.norm_sq(m.values) for e in gen)
+    cfg = P.SolverConfig(rank=k, tile_size=4, seed=3)
+    full = P.init_factors(v, d, cfg)
+    plan = ShardPlan(v, d, world)
+    out = {}
+    for name, engs in (("gen", gen), ("host", host)):
+        on_ranks(engs, lambda e, g: e.init_factors(cfg))
+        for g, e in enumerate(engs):
+            f = e.get_factors()
+            assert bits_equal(f.w, full.w[slice(*plan.v_range(g))])
+            assert bits_equal(f.ht, full.ht[slice(*plan.d_range(g))])
+        on_ranks(engs, lambda e, g: (e.precompute_h_products(), e.update_h(cfg, P.Algorithm.tiled),
+                                     e.precompute_w_products()))
+        out[name] = [(e.get_product("r"), e.get_product("p"), e.get_product("s")) for e in engs]
+    for a, b in zip(out["gen"], out["host"]):
+        assert all(bits_equal(x, y) for x, y in zip(a, b))
+    for e in gen + host:
+        e.close()
+
+
+def case_missing_rank_times_out(world):
+    m, w0, ht0 = conditioned_state(400, 300, 8, 0.05, 3)
+    engines = make_ranks(m, world, 8)
+    engines[0].set_timeout(0.5)
+    plan = ShardPlan(400, 300, 2)
+    engines[0].set_factors(P.FactorPair(w0[slice(*plan.v_range(0))], ht0[slice(*plan.d_range(0))]))
+    with pytest.raises(P.DeviceError, match="did not arrive"):
+        engines[0].precompute_h_products()  # rank 1 never pushed its W rows
+    for e in engines:
+        e.close()
+
+
+CASES = {f.__name__: f for f in (case_step_products_and_updates, case_iterate_matches_single_engine,
+                                  case_generated_shards, case_missing_rank_times_out)}
+
+
+def _run_case(name, world):
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    res = subprocess.run([sys.executable, str(Path(__file__).resolve()), name, str(world)], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_step_products_and_updates_match_the_restatement(gpu, world):
+    _run_case("case_step_products_and_updates", world)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_iterate_matches_single_engine(gpu, world):
+    _run_case("case_iterate_matches_single_engine", world)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_generated_shards_match_host_blocks_and_init(gpu, world):
+    _run_case("case_generated_shards", world)
+
+
+def test_missing_rank_times_out_instead_of_hanging(gpu):
+    _run_case("case_missing_rank_times_out", 2)
+
+
+def test_ranks_sharing_a_gpu_require_eager_loading(gpu):
+    env = dict(os.environ, CUDA_MODULE_LOADING="LAZY")
+    code = ("import sys; sys.path.insert(0, %r); from paper_1904_07935_b200 import plnmf as P; "
+            "from paper_1904_07935_b200.sharded import ShardEngine, connect_local\n"
+            "m = P.synth_csr(200, 100, 0.05, 1); e = [ShardEngine.from_csr(m, 2, g, 4) for g in range(2)]\n"
+            "try:\n    connect_local(e)\nexcept P.InvalidArgument as x:\n    print('refused:', x)\n")
+    res = subprocess.run([sys.executable, "-c", code % str(Path(__file__).resolve().parents[1])], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert "refused:" in res.stdout and "CUDA_MODULE_LOADING=EAGER" in res.stdout, res.stdout + res.stderr
+
+
+if __name__ == "__main__":
+    CASES[sys.argv[1]](int(sys.argv[2]))
+    print("ok")
