@@ -1,21 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark: FAST-HALS iterations/sec on the 20News-shaped sparse A at K=240
-(BASELINE.json metric; configs[1] = SURVEY.md C2), PL-NMF tiled algorithm,
-fp64, on the B200 engine.
+"""Benchmark: FAST-HALS iterations/sec (BASELINE.json metric), PL-NMF tiled
+algorithm, fp64, on the B200 engine.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference] [--workload c2|c5]
 
-A step is one FAST-HALS iteration (R=A^T W, S=W^T W, H update, P=A Ht,
-Q=Ht^T Ht, W update) with everything resident in HBM.  Each step is timed
-with CUDA events on the engine stream; L2 is flushed (a 512 MiB write) between
-steps, outside the timed interval.  N>1 runs N independent replicas (one
-process per GPU; C2 does not shard) and reports the max over
-ranks.  One JSON line is printed by rank 0.
+N = 1 (default): configs[1] = SURVEY.md C2, the 20News-shaped sparse A at
+K=240.  A step is one FAST-HALS iteration (R=A^T W, S=W^T W, H update, P=A Ht,
+Q=Ht^T Ht, W update) with everything resident in HBM, timed with CUDA events on
+the engine stream; L2 is flushed (a 512 MiB write) between steps, outside the
+timed interval.
+
+N > 1 (torchrun, one process per GPU): configs[4] = SURVEY.md C5 (2M x 1M, ~1e9
+nonzeros, K=256) on the sharded engine — W rows and Ht rows split over the
+ranks, the all-gathers and the per-column norm exchange over NVLink peer
+memory (csrc/shard_engine.cu).  One problem of fixed size: strong scaling;
+`--workload c5` runs the same engine on one GPU for the 1-GPU point.  The max
+over ranks of the device time is reported.  One JSON line, printed by rank 0.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 libplnmf compiled from the unmodified sources) on this host's cores, same
-workload and metric; its input comes from oracle/synth.c, so that arm never
-loads the engine library.
+workload and metric (C5: a 64x scaled C5-shaped sample, extrapolated); its
+input comes from oracle/synth.c, so that arm never loads the engine library.
 """
 from __future__ import annotations
 
@@ -176,9 +181,25 @@ def reference_sample(steps, warmup, tiled):
             f"unmodified sources, OpenMP on all host cores ({cpu_model()})")
 
 
-def reference_arm(args):
+def reference_arm(args, workload="c2"):
     # CPU-only: under torchrun rank 0 alone runs it, the other ranks exit 0 without work
     if int(os.environ.get("RANK", "0")) != 0:
+        return
+    if workload == "c5":
+        try:
+            val, cores, sample = time_reference_c5(steps=min(args.steps, 2))
+        except ImportError as e:
+            print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+            return
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s", "n_gpus": args.gpus,
+            "steps": min(args.steps, 2), "warmup": 1, "ms_per_step": 1e3 / val, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": c5_config(args.gpus), "extrapolated": f"x{C5_SAMPLE} from a scaled C5-shaped sample",
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "reference",
+                             "cpu": cpu_model(), "sample": sample},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
         return
     try:
         m = _RefCsr()
@@ -389,6 +410,152 @@ def ncu_traffic(kernel):
         return None
 
 
+# ----------------------------------------------------------------------------- C5: the sharded engine
+# 2M x 1M, density 5e-4 (~1e9 nonzeros, ~500 per row), K=256, T_auto=16;
+# W row-sharded over V, H over D (8(e)); every rank generates its blocks on the device.
+V5, D5, DENS5, K5, TILE5 = 2_000_000, 1_000_000, 5e-4, 256, 16
+C5_SAMPLE = 64  # reference arm: a C5-shaped instance scaled down 64x in rows and columns
+
+
+def c5_config(world, nnz=None):
+    return {"workload": f"C5: synthetic CSR {V5}x{D5}, density {DENS5} (~1e9 nonzeros), K={K5}, PL-NMF tile "
+                        f"{TILE5}, FAST-HALS iteration, W rows / Ht rows sharded over {world} GPU(s)",
+            "V": V5, "D": D5, "nnz": nnz, "K": K5, "tile_size": TILE5, "algorithm": "pl-nmf (tiled)",
+            "generator": f"splitmix64 geometric-gap Bernoulli rows, seed {GEN_SEED}, values U(0.1,2.0) fp32-rounded, "
+                         "generated on the device per rank",
+            "parallelism": f"row/column-sharded x{world} (peer-memory all-gathers + in-kernel norm exchange)",
+            "l2": "inputs larger than L2 (A 12 GB, W 4 GB): no flush"}
+
+
+def c5_arm(args):
+    """The large config through the sharded engine: one process per GPU, the
+    ranks connected over torch.distributed (IPC handles), one problem of fixed
+    size (strong scaling).  A step is one FAST-HALS iteration of the whole
+    problem; every rank times its run_iterations with CUDA events on its engine
+    stream and the max over ranks is reported."""
+    import torch
+    from paper_1904_07935_b200 import plnmf as P
+    from paper_1904_07935_b200.sharded import ShardEngine, connect
+
+    rank, world, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    t0 = time.perf_counter()
+    eng = ShardEngine.generate(V5, D5, DENS5, GEN_SEED, K5, world, rank, device=local)
+    if dist is not None:
+        connect(eng)  # IPC handles all-gathered, ||A||^2 chained over the ranks
+    else:
+        eng.set_norm_sq(eng.norm_sq_from(0.0))
+    setup_s = time.perf_counter() - t0
+    nnz_local = eng.nnz
+    nnz = int(allsum(dist, local, float(nnz_local)))
+    alg = P.Algorithm.tiled
+    cfg = P.SolverConfig(rank=K5, tile_size=TILE5, max_iters=1, rel_tol=0.0)
+    rng = np.random.default_rng(1000 + rank)  # synthetic factors: each rank's rows, U(1e-3, 1)
+    f0 = P.FactorPair(np.asfortranarray(rng.uniform(1e-3, 1.0, (eng.v, K5))),
+                      np.asfortranarray(rng.uniform(1e-3, 1.0, (eng.d, K5))))
+    eng.set_factors(f0)
+    for _ in range(args.warmup):
+        eng.run_iterations(cfg, alg, 1)
+    launches0 = eng.stats()["kernel_launches"]
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = eng.run_iterations(cfg, alg, args.steps)
+    torch.cuda.synchronize()
+    barrier(dist)
+    launches = eng.stats()["kernel_launches"] - launches0
+    phases = {k2: v2 / args.steps for k2, v2 in eng.phase_ms().items()}
+    total_ms = allmax(dist, local, ms)
+    value = args.steps / (total_ms * 1e-3)
+
+    # e2e through the public API with host factors: upload this rank's rows, iterate()
+    # (error evaluated every iteration, reference defaults), download
+    e2e_iters = 2
+    ecfg = P.SolverConfig(rank=K5, tile_size=TILE5, max_iters=e2e_iters, rel_tol=0.0, error_every=1)
+    barrier(dist)
+    t1 = time.perf_counter()
+    eng.set_factors(f0)
+    eng.iterate(ecfg, alg)
+    f1 = eng.get_factors()
+    e2e_s = allmax(dist, local, time.perf_counter() - t1)
+    fb = 8 * (eng.v + eng.d) * K5
+
+    # the SpMMs against HBM: P = A Ht gathers one K-wide operand row (2 KB) per nonzero from HBM
+    # (the operand is 2-4 GB, far beyond L2); the precompute_w phase also holds the Ht Gram
+    pk = peaks()
+    hbm = float(pk["hbm_gbs"])
+    gather = 8.0 * nnz_local * K5
+    pw_ms = phases["precompute_w"]
+    roofline = {"kernel": "spmm_csr (P = A_g Ht_full, this rank's row block; timed as the precompute_w phase, "
+                          "which also holds Q = gram(Ht_g))", "bound": "hbm",
+                "achieved": gather / (pw_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": gather / (pw_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                "algorithmic_bytes": gather, "bytes_definition": "nnz_local * K * 8 (operand-row gathers; "
+                "the compulsory 12 B/nonzero + factor bytes are ~1% of it)",
+                "launch_ms": pw_ms, "share_of_step": pw_ms / (total_ms / args.steps),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            val, cores, sample = time_reference_c5(steps=2)
+            cpu = {"value": val, "unit": "iters/s", "cores": cores, "kind": "reference", "cpu": cpu_model(),
+                   "sample": sample}
+        except ImportError as e:
+            cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": c5_config(world, nnz), "math": "exact", "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_iters / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": fb,
+                    "d2h_bytes_per_step": fb, "iters_per_step": e2e_iters,
+                    "what": "per rank: set_factors (this rank's W, Ht rows from host), iterate(max_iters=2, "
+                            "error_every=1, rel_tol=0), get_factors; host wall clock, max over ranks"},
+            "gpu_launches": launches, "clocks": clk.summary(), "phase_ms_per_step": phases,
+            "setup_s": setup_s, "nnz_per_rank": nnz_local,
+            "parallelism": f"sharded x{world}",
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def time_reference_c5(steps):
+    """The reference on a C5-shaped instance scaled down C5_SAMPLE x in rows and
+    columns with the same nonzeros per row (so nnz, the Grams and the updates
+    all scale by 1/C5_SAMPLE), timed like time_reference_cpu; the per-iteration
+    time is multiplied by C5_SAMPLE.  The sample's factors fit the host caches
+    far better than C5's, so the estimate favours the reference."""
+    from oracle.oracle import RefInput, ref, ref_init_factors, ref_iterate, synth_csr
+    v, d = V5 // C5_SAMPLE, D5 // C5_SAMPLE
+    rp, ci, val = synth_csr(v, d, DENS5 * C5_SAMPLE, GEN_SEED)
+    a = RefInput(v, d, rp, ci, val)
+    w, ht = ref_init_factors(v, d, K5, seed=0)
+    cores = ref().ref_max_threads()
+    n = 1 + steps
+    _, _, tr = ref_iterate(a, w, ht, K5, max_iters=n, rel_tol=0.0, error_every=1, tile=TILE5, tiled=True)
+    rec = tr["records"]
+    el = rec[:, 2]
+    per = [(el[i] - el[i - 1]) - rec[i, 11] for i in range(1, n)]
+    spi = float(np.mean(per)) * C5_SAMPLE
+    sample = (f"{steps} PL-NMF (T={TILE5}) iterations of a C5-shaped {v}x{d} instance ({int(rp[-1])} nonzeros, "
+              f"~{DENS5 * C5_SAMPLE * d:.0f} per row as in C5), K={K5}, after 1 discarded; per iteration = wall delta "
+              f"- error_eval, x{C5_SAMPLE} (every phase is linear in rows at fixed nonzeros per row); oracle/_ref "
+              f"on all host cores ({cpu_model()})")
+    return 1.0 / spi, cores, sample
+
+
+def allsum(dist, local, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -398,11 +565,17 @@ def main():
     ap.add_argument("--math", default="exact", choices=["exact", "fused"])
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default=None, choices=["c2", "c5"],
+                    help="default: C2 on 1 GPU (the metric's config), the sharded C5 on N > 1 GPUs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    workload = args.workload or ("c5" if max(world, args.gpus) > 1 else "c2")
     if args.impl == "reference":
-        reference_arm(args)
+        reference_arm(args, workload)
+    elif workload == "c5":
+        c5_arm(args)
     else:
         engine_arm(args)
 

@@ -181,8 +181,38 @@ def case_missing_rank_times_out(world):
         e.close()
 
 
+def case_ipc_rank(world):
+    """One rank of a multi-process run (one process per rank, all on cuda:0):
+    torch.distributed (gloo) all-gathers the windows' CUDA IPC handles
+    (sharded.connect) — the launch path of one process per GPU.  Without MPS
+    the ranks' contexts time-slice the GPU, so the in-kernel waits span
+    context switches: slow, but the protocol is the multi-GPU one."""
+    import torch.distributed as dist
+    from paper_1904_07935_b200.sharded import connect
+    rank = int(os.environ["RANK"])
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, w0, ht0 = conditioned_state(400, 300, 8, 0.05, 3)
+        plan = ShardPlan(400, 300, world)
+        e = ShardEngine.from_csr(m, world, rank, 8)
+        e.set_timeout(120.0)
+        connect(e, chain_norm=False)
+        e.set_factors(P.FactorPair(w0[slice(*plan.v_range(rank))], ht0[slice(*plan.d_range(rank))]))
+        cfg = P.SolverConfig(rank=8, tile_size=3)
+        e.precompute_h_products()
+        e.update_h(cfg, P.Algorithm.tiled)
+        e.precompute_w_products()
+        e.update_w(cfg, P.Algorithm.tiled)
+        rep = e.evaluate_error()
+        f = e.get_factors()
+        np.savez(os.environ["OUT"] + f"_r{rank}.npz", w=f.w, ht=f.ht, err=rep.relative, q=e.get_product("q"))
+        e.close()
+    finally:
+        dist.destroy_process_group()
+
+
 CASES = {f.__name__: f for f in (case_step_products_and_updates, case_iterate_matches_single_engine,
-                                  case_generated_shards, case_missing_rank_times_out)}
+                                  case_generated_shards, case_missing_rank_times_out, case_ipc_rank)}
 
 
 def _run_case(name, world):
@@ -209,6 +239,36 @@ def test_generated_shards_match_host_blocks_and_init(gpu, world):
 
 def test_missing_rank_times_out_instead_of_hanging(gpu):
     _run_case("case_missing_rank_times_out", 2)
+
+
+def test_two_processes_connected_over_cuda_ipc(gpu, tmp_path):
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    world = 2
+    procs = []
+    for g in range(world):
+        env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", RANK=str(g), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), OUT=str(tmp_path / "ipc"))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), "case_ipc_rank", str(world)],
+                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(o[-3000:] for o in outs)
+    got = [np.load(tmp_path / f"ipc_r{g}.npz") for g in range(world)]
+    # the same arithmetic as the in-process ranks: the sharded restatement
+    m, w0, ht0 = conditioned_state(400, 300, 8, 0.05, 3)
+    plan = ShardPlan(400, 300, world)
+    trp, tci, tval = R.transpose(400, 300, m.row_ptr, m.col_idx, m.values)
+    s_sh = ordered_sum([R.gram(np.ascontiguousarray(w0[slice(*plan.v_range(g))])) for g in range(world)])
+    ht1, _ = R.update_tiled(ht0, s_sh, R.spmm(300, 400, trp, tci, tval, w0), 3, is_w=False)
+    q_sh = ordered_sum([R.gram(np.ascontiguousarray(ht1[slice(*plan.d_range(g))])) for g in range(world)])
+    w1, _ = R.update_tiled(w0, q_sh, R.spmm(400, 300, m.row_ptr, m.col_idx, m.values, ht1), 3, is_w=True)
+    for g in range(world):
+        assert bits_equal(got[g]["ht"], ht1[slice(*plan.d_range(g))])
+        assert bits_equal(got[g]["q"], q_sh)
+    assert rel_max(w1, np.concatenate([x["w"] for x in got])) <= 1e-12
+    assert float(got[0]["err"]) == float(got[1]["err"])
 
 
 def test_ranks_sharing_a_gpu_require_eager_loading(gpu):
