@@ -213,6 +213,10 @@ plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthrea
  * per-SM rows do not fit the persistent kernel (C5), so its parity can be
  * tested on small inputs.  Results are those of the same T either way. */
 plnmf_status plnmf_gpu_force_streaming(plnmf_gpu_engine* e, int32_t on);
+/* Verification hook: the SpMMs take the column-blocked path (spmm.cu) with blocks of
+ * `operand_rows` operand rows whenever the operand is larger (0: automatic — blocks of
+ * ~48 MB for operands over ~96 MB).  Results are bit-identical either way. */
+plnmf_status plnmf_gpu_force_spmm_blocks(plnmf_gpu_engine* e, int64_t operand_rows);
 
 /* FactorPair in/out (proj/include/plnmf/workspace.hpp:32-35). */
 plnmf_status plnmf_gpu_set_factors(plnmf_gpu_engine* e, const double* w_colmajor,

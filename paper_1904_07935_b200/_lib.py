@@ -70,6 +70,7 @@ SIGNATURES = {
     "plnmf_gpu_set_math": (C.c_int, [Engine_p, C.c_int]),
     "plnmf_gpu_set_reference_threads": (C.c_int, [Engine_p, i32]),
     "plnmf_gpu_force_streaming": (C.c_int, [Engine_p, i32]),
+    "plnmf_gpu_force_spmm_blocks": (C.c_int, [Engine_p, i64]),
     "plnmf_gpu_set_factors": (C.c_int, [Engine_p, P_f64, P_f64]),
     "plnmf_gpu_get_factors": (C.c_int, [Engine_p, P_f64, P_f64]),
     "plnmf_gpu_init_factors": (C.c_int, [Engine_p, P_cfg]),

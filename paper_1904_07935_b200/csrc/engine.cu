@@ -88,6 +88,10 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     e->staging = dalloc<double>(e, std::max(std::max(v, d), k) * k);  // factors and K x K products
     e->counters = dalloc<unsigned>(e, kern::exchange_counters(k));
     e->totals = dalloc<double>(e, k);
+    if (e->sparse) {  // column-blocked SpMM cursors (operands far larger than L2)
+        e->cursor_p = dalloc<int64_t>(e, v);
+        e->cursor_r = dalloc<int64_t>(e, d);
+    }
     PLNMF_CUDA_CHECK(cudaMallocHost(&e->host_scalars, sizeof(double) * 8));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->norms, 0, sizeof(double) * k, e->s));
     PLNMF_CUDA_CHECK(cudaMemsetAsync(e->p, 0, sizeof(double) * v * k, e->s));
@@ -143,6 +147,10 @@ void tensor_at_w(plnmf_gpu_engine* e) {
 }
 
 // ---- products ------------------------------------------------------------------------
+// rows of the gathered operand of R = A^T W / P = A Ht (a shard's padded full factor)
+int64_t operand_rows_w(const plnmf_gpu_engine* e) { return e->shard ? e->world * e->vcap : e->v; }
+int64_t operand_rows_h(const plnmf_gpu_engine* e) { return e->shard ? e->world * e->dcap : e->d; }
+
 // R = A^T W then S = W^T W, one after the other on the engine stream (S is
 // skipped when the last error evaluation already left gram(W) in S: same W,
 // same deterministic kernel, same bits — the reference recomputes it,
@@ -162,7 +170,8 @@ void precompute_h(plnmf_gpu_engine* e) {
             plnmf::shard::wait(e, plnmf::kChanW);
             w = plnmf::shard::w_full(e);
         }
-        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, w, e->k, e->r, e->nnz_t);
+        e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, w, e->k, e->r, e->nnz_t,
+                                      operand_rows_w(e), e->cursor_r, e->spmm_block);
     } else if (e->tensor) {
         tensor_at_w(e);
     } else {
@@ -182,7 +191,8 @@ void precompute_w(plnmf_gpu_engine* e) {
             plnmf::shard::wait(e, plnmf::kChanHt);
             ht = plnmf::shard::ht_full(e);
         }
-        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, ht, e->k, e->p, e->nnz);
+        e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, ht, e->k, e->p, e->nnz,
+                                      operand_rows_h(e), e->cursor_p, e->spmm_block);
     } else if (e->tensor) {
         tensor_a_ht(e);
     } else {
@@ -412,7 +422,8 @@ ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
     if (ahead_r) {
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
-        e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next);
+        e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next, e->nnz_t,
+                                      operand_rows_w(e), e->cursor_r, e->spmm_block);
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
         e->r_valid = true;
     }
@@ -917,6 +928,14 @@ plnmf_status plnmf_gpu_force_streaming(plnmf_gpu_engine* e, int32_t on) {
     });
 }
 
+plnmf_status plnmf_gpu_force_spmm_blocks(plnmf_gpu_engine* e, int64_t operand_rows) {
+    return guarded([&] {
+        check_engine(e);
+        if (operand_rows < 0) throw std::invalid_argument("plnmf_gpu_force_spmm_blocks: negative block");
+        e->spmm_block = operand_rows;
+    });
+}
+
 plnmf_status plnmf_gpu_set_reference_threads(plnmf_gpu_engine* e, int32_t nthreads) {
     return guarded([&] {
         check_engine(e);
@@ -1131,12 +1150,12 @@ plnmf_status plnmf_gpu_time_kernel(plnmf_gpu_engine* e, const plnmf_config* cfg,
         auto once = [&] {
             switch (which) {
                 case 0:
-                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p, e->nnz);
+                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p, e->nnz, e->d, e->cursor_p, e->spmm_block);
                     else if (e->tensor) tensor_a_ht(e);
                     else e->launches += kern::dense_a_ht(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->ht, e->p);
                     break;
                 case 1:
-                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r);
+                    if (e->sparse) e->launches += kern::spmm_csr(e->s, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r, e->nnz_t, e->v, e->cursor_r, e->spmm_block);
                     else if (e->tensor) tensor_at_w(e);
                     else e->launches += kern::dense_at_w(e->s, e->math, e->v, e->d, e->k, e->a_dense, e->w, e->r);
                     break;

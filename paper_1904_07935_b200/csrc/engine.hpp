@@ -38,6 +38,8 @@ struct plnmf_gpu_engine {
     double *w = nullptr, *ht = nullptr, *w_new = nullptr, *h_new = nullptr;
     double *p = nullptr, *q = nullptr, *r = nullptr, *sm = nullptr, *norms = nullptr;
     double* r_next = nullptr;  // R of the current W computed ahead (iterate), swapped into r when used
+    int64_t *cursor_p = nullptr, *cursor_r = nullptr;  // column-blocked SpMM cursors (spmm.cu)
+    int64_t spmm_block = 0;  // > 0: column blocks of this many operand rows (verification hook)
     double *gram_scratch = nullptr, *partials = nullptr, *dot_partials = nullptr;
     double *scalars = nullptr;  // [0] pw, [1] sq, [2..4] error report, [5] direct sum
     double *staging = nullptr, *direct_partials = nullptr;

@@ -407,6 +407,11 @@ class Engine:
         """Verification hook: tiled updates take the streaming plan (stream.cu)."""
         _check(L.lib().plnmf_gpu_force_streaming(self._h, int(bool(on))))
 
+    def force_spmm_blocks(self, operand_rows: int) -> None:
+        """Verification hook: column-blocked SpMMs (spmm.cu) with blocks of
+        `operand_rows` operand rows (0: automatic, operands beyond ~96 MB)."""
+        _check(L.lib().plnmf_gpu_force_spmm_blocks(self._h, int(operand_rows)))
+
     def set_reference_threads(self, n: int) -> None:
         """Math.reference_order: the reference's OpenMP team size (its tiled
         norm partials depend on it, proj/src/tiled.cpp:97-99)."""

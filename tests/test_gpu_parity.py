@@ -46,6 +46,22 @@ def test_spmm_both_directions_bitwise(gpu, k):
     assert bits_equal(eng.get_product("r"), r_ref)
 
 
+@pytest.mark.parametrize("k,block", [(2, 1), (24, 37), (240, 100), (256, 977), (64, 1499), (30, 3000)])
+def test_spmm_column_blocked_bitwise(gpu, k, block):
+    """The column-blocked SpMM (operands beyond L2, spmm.cu) carries each output's
+    running sum through y from block to block: bit-identical to the oracle for
+    any block size, including blocks a row has no entries in and empty rows."""
+    m, eng, f = make(3000, 1500, 0.01, k)
+    rp = m.row_ptr.copy()
+    eng.force_spmm_blocks(block)
+    eng.precompute_w_products()
+    eng.precompute_h_products()
+    trp, tci, tval = ref_at(m)
+    assert bits_equal(eng.get_product("p"), R.spmm(m.rows, m.cols, m.row_ptr, m.col_idx, m.values, f.ht))
+    assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, f.w))
+    assert np.array_equal(rp, m.row_ptr)
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 2047, 2048, 2049, 5001])
 @pytest.mark.parametrize("k", [1, 5, 33, 64])
 def test_gram_bitwise(gpu, n, k):
