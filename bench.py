@@ -480,20 +480,28 @@ def c5_arm(args):
     e2e_s = allmax(dist, local, time.perf_counter() - t1)
     fb = 8 * (eng.v + eng.d) * K5
 
-    # the SpMMs against HBM: P = A Ht gathers one K-wide operand row (2 KB) per nonzero from HBM
-    # (the operand is 2-4 GB, far beyond L2); the precompute_w phase also holds the Ht Gram
+    # P = A_g Ht_full (the precompute_w phase, which also holds Q = gram(Ht_g)) against HBM with its
+    # compulsory bytes, and its operand-row gathers (one K-wide row per nonzero) against the measured
+    # L2 gather peak: the column-blocked SpMM (spmm.cu) keeps each block's operand rows in L2
     pk = peaks()
     hbm = float(pk["hbm_gbs"])
-    gather = 8.0 * nnz_local * K5
     pw_ms = phases["precompute_w"]
-    roofline = {"kernel": "spmm_csr (P = A_g Ht_full, this rank's row block; timed as the precompute_w phase, "
-                          "which also holds Q = gram(Ht_g))", "bound": "hbm",
-                "achieved": gather / (pw_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": gather / (pw_ms * 1e-3) / 1e9 / hbm, "traffic": None,
-                "algorithmic_bytes": gather, "bytes_definition": "nnz_local * K * 8 (operand-row gathers; "
-                "the compulsory 12 B/nonzero + factor bytes are ~1% of it)",
+    b_alg = 12.0 * nnz_local + 8.0 * (eng.v + 1) + 8.0 * D5 * K5 + 8.0 * eng.v * K5
+    gather = 8.0 * nnz_local * K5
+    l2 = l2_peak()
+    rate = b_alg / (pw_ms * 1e-3) / 1e9
+    roofline = {"kernel": "spmm_blocked_kernel (P = A_g Ht_full, column-blocked; timed as the precompute_w "
+                          "phase, which also holds Q = gram(Ht_g))", "bound": "hbm",
+                "achieved": rate, "peak": hbm, "unit": "GB/s", "frac": rate / hbm,
+                "traffic": ncu_traffic("c5_spmm_per_spmm"), "algorithmic_bytes": b_alg,
+                "bytes_definition": "12 B per nonzero + row pointers + the operand read once + P written once",
                 "launch_ms": pw_ms, "share_of_step": pw_ms / (total_ms / args.steps),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback"}
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not pk.get("_fallback") else "fallback",
+                "l2_gather": {"bytes": gather, "GBps": gather / (pw_ms * 1e-3) / 1e9,
+                              "peak_GBps": l2.get("gather_l2_gbs_16B"),
+                              "frac": (gather / (pw_ms * 1e-3) / 1e9 / l2["gather_l2_gbs_16B"])
+                              if l2.get("gather_l2_gbs_16B") else None,
+                              "peak_source": "profiles/l2_peak.json (tools/l2bw_bench.cu on a B200)"}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

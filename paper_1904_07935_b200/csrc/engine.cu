@@ -541,22 +541,31 @@ void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, 
         PLNMF_CUDA_CHECK(cudaEventRecord(ev[3], e->s));
         update_w(e, cfg, alg);
         PLNMF_CUDA_CHECK(cudaEventRecord(ev[4], e->s));
-        PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
+        const bool eval = it % cfg.error_every == 0;
+        // The error evaluation is queued right behind the W update (its own readback is the
+        // iteration's one host synchronisation); the phase times are read after it.
+        if (!eval) PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
         plnmf_phase_times ph{};
-        ph.precompute_h = elapsed_s(ev[0], ev[1]);
-        ph.precompute_w = elapsed_s(ev[2], ev[3]);
-        if (tiled) {
-            // one fused look-ahead kernel per update (init, phases 1-3, normalisation)
-            ph.phase2 = elapsed_s(ev[1], ev[2]) + elapsed_s(ev[3], ev[4]);
-        } else {
-            ph.update_h = elapsed_s(ev[1], ev[2]);
-            ph.update_w = elapsed_s(ev[3], ev[4]);
-        }
-        if (it % cfg.error_every == 0) {
-            te = clock::now();
+        auto phase_times = [&] {
+            ph.precompute_h = elapsed_s(ev[0], ev[1]);
+            ph.precompute_w = elapsed_s(ev[2], ev[3]);
+            if (tiled) {
+                // one fused look-ahead kernel per update (init, phases 1-3, normalisation)
+                ph.phase2 = elapsed_s(ev[1], ev[2]) + elapsed_s(ev[3], ev[4]);
+            } else {
+                ph.update_h = elapsed_s(ev[1], ev[2]);
+                ph.update_w = elapsed_s(ev[3], ev[4]);
+            }
+        };
+        if (eval) {
             // next iteration's R = A^T W computed ahead (unused if the loop stops)
             const ErrorReport rep = evaluate_error(e, e->sparse && !e->shard && it < cfg.max_iters);
-            ph.error_eval = since(te);
+            PLNMF_CUDA_CHECK(cudaEventRecord(ev[5], e->s));
+            PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[5]));
+            phase_times();
+            // the evaluation's own time (from the end of the W update to its readback), not the
+            // update work the host call waited behind
+            ph.error_eval = elapsed_s(ev[4], ev[5]);
             add_times(totals, ph);
             if (!std::isfinite(rep.rel))
                 throw plnmf::NonFinite("iterate: objective became non-finite at iteration " + std::to_string(it));
@@ -574,6 +583,7 @@ void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, 
             }
             prev = rep.rel;
         } else {
+            phase_times();
             add_times(totals, ph);
         }
     }
