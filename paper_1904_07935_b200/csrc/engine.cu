@@ -216,6 +216,13 @@ void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
         e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device, e->force_streaming);
     }
     e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device, e->force_streaming);
+    if (e->plan_w.streaming) {  // the W update's column-major tile scratch (stream_w_kernel)
+        const int64_t xn = kern::stream_w_scratch_doubles(e->plan_w, tile);
+        if (xn > e->wscratch_n) {
+            e->wscratch = dalloc<double>(e, xn);
+            e->wscratch_n = xn;
+        }
+    }
     const int64_t qn = kern::qpanel_doubles(e->k, tile);
     if (qn > e->qpanel_n) {
         e->qpanel = dalloc<double>(e, qn);
@@ -341,7 +348,7 @@ void update_w_shard(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorith
     ensure_plans(e, cfg.tile_size);
     const plnmf::WorldXch x = plnmf::shard::next_exchange(e);
     e->launches += kern::stream_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true, e->w,
-                                       e->w_new, e->q, e->p, e->norms, e->partials, e->counters, &x);
+                                       e->w_new, e->q, e->p, e->norms, e->partials, e->counters, &x, e->wscratch);
     std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
     e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);
     plnmf::shard::push_factor(e, plnmf::kChanW);
@@ -358,7 +365,7 @@ void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         long long* prof = prof_buffer(e, e->plan_w.grid);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true,
                                           e->w, e->w_new, e->q, e->p, e->norms, e->partials, e->counters, e->totals,
-                                          prof, e->qpanel);
+                                          prof, e->qpanel, e->wscratch);
         if (prof) prof_report(e, "W update", e->plan_w.grid);
         std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
         e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);

@@ -65,6 +65,8 @@ struct plnmf_gpu_engine {
     std::vector<cudaEvent_t> events;  // per-phase timing pool
     long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
     int64_t prof_n = 0;
+    double* wscratch = nullptr;       // streaming W update: column-major tile scratch (stream.cu)
+    int64_t wscratch_n = 0;
     double* qpanel = nullptr;         // coeff column panels of the tiled updates
     int64_t qpanel_n = 0;
 

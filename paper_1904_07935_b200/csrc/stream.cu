@@ -105,10 +105,10 @@ struct StreamArgs {
     double* partials;
     unsigned* counters;
     WorldXch xch;  // WORLD: the other ranks' windows (sharded engine)
+    double* xs;    // stream_w_kernel: per-CTA column-major tile scratch, 3 x tile x ldx doubles per CTA
+    int64_t ldx;
 };
 
-// WORLD: the sharded W update — the column's sum is the rank-local grid sum
-// followed by the cross-rank exchange over peer memory (peer.cuh: world_sum).
 template <class M, bool NORMALIZE, bool WORLD = false>
 __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs p) {
     __shared__ double red[48];
@@ -200,6 +200,195 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs 
     }
 }
 
+// The W update of the streaming plan with its phase 2 on a column-major copy of
+// the tile.  Phase 2 needs, for every column t, all w tile values of every row
+// (new for j < t, old for j >= t, tiled.cpp:103-128).  Read from the row-major
+// factor those are 32 scattered rows per warp load, re-fetched for every
+// column (ncu at C5: 361 GB of DRAM traffic per update for 12 GB of compulsory
+// bytes).  Here each CTA first copies its rows' tile into X (old values, then
+// overwritten in place by the new values: exactly the operands the reference
+// reads), the accumulators into AC and the additive term into AD, all
+// column-major, so every phase-2 load is a coalesced column read; the finished
+// tile is copied back to the row-major factor before phase 3.  Same
+// per-element operation order as stream_update_kernel.
+constexpr int kSWarps = kSThreads / kWarp;
+
+template <class M, bool WORLD>
+__global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
+    __shared__ double red[48];
+    // dynamic: phase 3's negated coefficient rows (w x (k - e)); the transposes' per-warp stages
+    // (T x 33 each) — never live at the same time
+    extern __shared__ __align__(16) double cq[];
+    const int k = p.k, T = p.tile, tid = threadIdx.x;
+    const int warp = tid / kWarp, lane = lane_id();
+    double* st = cq + (int64_t)warp * T * (kWarp + 1);
+    const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_cta;
+    const int64_t r1 = (r0 + p.rows_per_cta < p.n) ? r0 + p.rows_per_cta : p.n;
+    const int64_t nl = r1 > r0 ? r1 - r0 : 0;
+    const int64_t ld = p.ldx;
+    double* X = p.xs + (int64_t)blockIdx.x * 3 * T * ld;
+    double* AC = X + (int64_t)T * ld;
+    double* AD = AC + (int64_t)T * ld;
+    for (int b = 0; b < k; b += T) {
+        const int e = (b + T < k) ? b + T : k, w = e - b;
+        // ---- the tile, column-major: each warp transposes 32-row chunks through its own
+        // shared-memory stage (row segments in, coalesced 32-row column pieces out)
+        for (int64_t i0 = (int64_t)warp * kWarp; i0 < nl; i0 += (int64_t)kSWarps * kWarp) {
+            const double* src[3] = {p.old_m, p.nb, p.add};
+            double* dst[3] = {X, AC, AD};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                for (int idx = lane; idx < kWarp * w; idx += kWarp) {
+                    const int ii = idx / w, j = idx - ii * w;
+                    if (i0 + ii < nl) st[j * (kWarp + 1) + ii] = src[a][(r0 + i0 + ii) * k + b + j];
+                }
+                __syncwarp();
+                if (i0 + lane < nl)
+                    for (int j = 0; j < w; ++j) dst[a][j * ld + i0 + lane] = st[j * (kWarp + 1) + lane];
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // ---- phase 2: columns in order; each thread keeps the same rows throughout
+        for (int t = b; t < e; ++t) {
+            const int tt = t - b;
+            double ss = 0.0;
+            if (w <= 16) {
+                double c[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) c[j] = (j < w) ? __ldg(p.coeff + (int64_t)(b + j) * k + t) : 0.0;
+                for (int64_t i = tid; i < nl; i += kSThreads) {
+                    double x[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) x[j] = (j < w) ? X[j * ld + i] : 0.0;
+                    double s = 0.0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < w) s = M::madd(s, x[j], c[j]);
+                    const double val = clamp_floor(p.eps, dsub(dadd(AC[tt * ld + i], AD[tt * ld + i]), s));
+                    X[tt * ld + i] = val;
+                    ss = M::madd(ss, val, val);
+                }
+            } else {
+                for (int64_t i = tid; i < nl; i += kSThreads) {
+                    double s = 0.0;
+                    for (int j0 = 0; j0 < w; j0 += 8) {
+                        double x[8], c[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = j0 + u;
+                            x[u] = (j < w) ? X[j * ld + i] : 0.0;
+                            c[u] = (j < w) ? __ldg(p.coeff + (int64_t)(b + j) * k + t) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (j0 + u < w) s = M::madd(s, x[u], c[u]);
+                    }
+                    const double val = clamp_floor(p.eps, dsub(dadd(AC[tt * ld + i], AD[tt * ld + i]), s));
+                    X[tt * ld + i] = val;
+                    ss = M::madd(ss, val, val);
+                }
+            }
+            const double blk = block_sum(ss, red);
+            if (tid < kWarp) {
+                const double nrm =
+                    WORLD ? __dsqrt_rn(world_sum(grid_exchange_sum(blk, t, gridDim.x, p.partials, p.counters), t, p.xch))
+                          : grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
+                if (tid == 0) {
+                    red[40] = nrm;
+                    if (blockIdx.x == 0) p.norms[t] = nrm;
+                }
+            }
+            __syncthreads();
+            const double norm = red[40];
+            for (int64_t i = tid; i < nl; i += kSThreads)
+                X[tt * ld + i] = clamp_floor(p.eps, __ddiv_rn(X[tt * ld + i], norm));  // tiled.cpp:146
+        }
+        // ---- phase 3 (tiled.cpp:158-174): nb(r, c) += (-coeff(b+j, c)) * new(r, b+j), j ascending,
+        // for every c >= e.  One thread per row: the row's w new values (a coalesced column read of X)
+        // stay in registers for all its columns; the tile's coefficient rows are staged in shared
+        // memory (every thread reads the same entry: broadcast); 4 columns of the row per step
+        // (32-byte sector-sized accesses of the row-major factor).
+        if (e < k) {
+            const int rest = k - e;
+            for (int idx = tid; idx < w * rest; idx += kSThreads) {
+                const int j = idx / rest, c = idx - j * rest;
+                cq[j * rest + c] = -1.0 * p.coeff[(int64_t)(b + j) * k + e + c];
+            }
+            __syncthreads();
+            const bool vec4 = (k % 2 == 0) && (e % 2 == 0);
+            for (int64_t i = tid; i < nl; i += kSThreads) {
+                double x[16];
+                const bool small = w <= 16;
+                if (small) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) x[j] = (j < w) ? X[j * ld + i] : 0.0;
+                }
+                double* row = p.nb + (r0 + i) * k + e;
+                auto load4 = [&](int c0, double (&a)[4]) {
+                    if (c0 + 4 <= rest && vec4) {
+                        const double2 lo = *reinterpret_cast<const double2*>(row + c0);
+                        const double2 hi = *reinterpret_cast<const double2*>(row + c0 + 2);
+                        a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) a[u] = (c0 + u < rest) ? row[c0 + u] : 0.0;
+                    }
+                };
+                double an[4];
+                load4(0, an);
+                for (int c0 = 0; c0 < rest; c0 += 4) {
+                    double a[4];
+                    const bool full = c0 + 4 <= rest;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) a[u] = an[u];
+                    if (c0 + 4 < rest) load4(c0 + 4, an);  // the next group's loads in flight during this one
+                    if (small) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < w) {
+                                const double* q = cq + j * rest + c0;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+                                    if (c0 + u < rest) a[u] = M::madd(a[u], q[u], x[j]);
+                            }
+                        }
+                    } else {
+                        for (int j = 0; j < w; ++j) {
+                            const double xj = X[j * ld + i];
+                            const double* q = cq + j * rest + c0;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (c0 + u < rest) a[u] = M::madd(a[u], q[u], xj);
+                        }
+                    }
+                    if (full && vec4) {
+                        *reinterpret_cast<double2*>(row + c0) = make_double2(a[0], a[1]);
+                        *reinterpret_cast<double2*>(row + c0 + 2) = make_double2(a[2], a[3]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (c0 + u < rest) row[c0 + u] = a[u];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- the finished tile back to the row-major factor (the same warp-level transpose)
+        for (int64_t i0 = (int64_t)warp * kWarp; i0 < nl; i0 += (int64_t)kSWarps * kWarp) {
+            if (i0 + lane < nl)
+                for (int j = 0; j < w; ++j) st[j * (kWarp + 1) + lane] = X[j * ld + i0 + lane];
+            __syncwarp();
+            for (int idx = lane; idx < kWarp * w; idx += kWarp) {
+                const int ii = idx / w, j = idx - ii * w;
+                if (i0 + ii < nl) p.nb[(r0 + i0 + ii) * k + b + j] = st[j * (kWarp + 1) + ii];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+}
+
 int sm_count(int device) {
     int n = 0;
     PLNMF_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
@@ -238,9 +427,14 @@ PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize
     return plan;
 }
 
+int64_t stream_w_scratch_doubles(const PhaseBPlan& plan, int64_t tile) {
+    return (int64_t)plan.grid * 3 * tile * plan.rows_per_cta;
+}
+
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
-                  const double* add, double* norms, double* partials, unsigned* counters, const WorldXch* xch) {
+                  const double* add, double* norms, double* partials, unsigned* counters, const WorldXch* xch,
+                  double* scratch) {
     if (n <= 0 || k <= 0) return 0;
     // phase A: init + phase 1 into `out` (used as the accumulator nb)
     const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
@@ -250,22 +444,35 @@ int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int
         stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
     PLNMF_CUDA_CHECK(cudaGetLastError());
     const bool world = xch && xch->world > 1;
+    // stream_w_kernel: tiles up to 32 wide; shared memory for the coefficient rows and the stages
+    const size_t w_smem = sizeof(double) * (size_t)std::max<int64_t>(tile * k, (int64_t)kSWarps * tile * (kWarp + 1));
+    if (scratch && (tile > 32 || w_smem > 200 * 1024)) scratch = nullptr;
     StreamArgs a{n, (int)k, (int)tile, eps, plan.rows_per_cta, old_m, out, coeff, add, norms, partials, counters,
-                 world ? *xch : WorldXch{}};
+                 world ? *xch : WorldXch{}, scratch, plan.rows_per_cta};
     const dim3 grid((unsigned)plan.grid), block(kSThreads);
     if (w_update) {
         exchange_reset(s, k, plan.grid, partials, counters);
         void* args[] = {&a};
-        const void* fn = world ? ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true, true>
-                                                     : (const void*)stream_update_kernel<MathFused, true, true>)
-                               : ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
-                                                     : (const void*)stream_update_kernel<MathFused, true>);
+        const void* fn;
+        if (scratch)  // column-major tile scratch (stream_w_kernel)
+            fn = world ? ((m == Math::exact) ? (const void*)stream_w_kernel<MathExact, true>
+                                             : (const void*)stream_w_kernel<MathFused, true>)
+                       : ((m == Math::exact) ? (const void*)stream_w_kernel<MathExact, false>
+                                             : (const void*)stream_w_kernel<MathFused, false>);
+        else
+            fn = world ? ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true, true>
+                                             : (const void*)stream_update_kernel<MathFused, true, true>)
+                       : ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
+                                             : (const void*)stream_update_kernel<MathFused, true>);
         // a plan with fewer CTAs than SMs (ranks sharing one GPU) is co-resident with
         // the other ranks' kernels only under a plain launch
+        // stream_w_kernel: the tile's coefficient rows for phase 3 in dynamic shared memory
+        const size_t smem = scratch ? w_smem : 0;
+        if (smem > 48 * 1024) PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (plan.cooperative)
-            PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+            PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s));
         else
-            PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, 0, s));
+            PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, smem, s));
     } else if (m == Math::exact) {
         stream_update_kernel<MathExact, false><<<grid, block, 0, s>>>(a);
     } else {

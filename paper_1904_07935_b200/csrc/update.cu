@@ -262,11 +262,11 @@ int64_t qpanel_doubles(int64_t k, int64_t tile) {
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
-                 long long* prof, double* qpanel) {
+                 long long* prof, double* qpanel, double* stream_scratch) {
     if (n <= 0 || k <= 0) return 0;
     if (plan.streaming)
         return stream_update(s, m, plan, n, k, tile, eps, w_update, old_m, out, coeff, add, norms, partials,
-                             counters);
+                             counters, nullptr, w_update ? stream_scratch : nullptr);
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
                norms, partials, counters, totals, prof, knob("PLNMF_NO_OVERLAP") ? 0 : knob("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1,
                nullptr, qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
