@@ -51,6 +51,18 @@ __device__ __forceinline__ void decode_upper(int p, int ntile, int& ta, int& tb)
 // (lane0 + 0.0) + lane1 exactly like the compiled reduction.
 // TJ: entries per thread along b (4: 64 threads per CTA; 2: 128 threads, for short
 // matrices whose (tile, block, lane) count leaves SMs under-occupied)
+// DIAG (a diagonal tile, ta == tb): register entries (i, j) that lie below the
+// diagonal for every thread of the CTA are not computed (the combine kernel
+// reads only a <= b) — a quarter to three eighths of a diagonal tile's work.
+template <int TJ, int TI>
+__host__ __device__ constexpr bool below_diag(int i, int j) {
+    return (32 / TI) * i > (32 / TJ - 1) + (32 / TJ) * j;
+}
+
+template <class M, int TJ, int TI, bool DIAG>
+__device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __restrict__ m, double* __restrict__ part,
+                                          int ta, int tb, double (&As)[2][32][32], double (&Bs)[2][32][32]);
+
 template <class M, int TJ = 4, int TI = 4>
 __global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(int64_t n, int k,
                                                                   const double* __restrict__ m,
@@ -63,6 +75,13 @@ __global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(in
     __shared__ __align__(16) double Bs[2][kGramChunk][kGramTile];
     int ta, tb;
     decode_upper(blockIdx.x, ntile, ta, tb);
+    if (ta == tb) gram_tile<M, TJ, TI, true>(n, k, m, part, ta, tb, As, Bs);
+    else gram_tile<M, TJ, TI, false>(n, k, m, part, ta, tb, As, Bs);
+}
+
+template <class M, int TJ, int TI, bool DIAG>
+__device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __restrict__ m, double* __restrict__ part,
+                                          int ta, int tb, double (&As)[2][32][32], double (&Bs)[2][32][32]) {
     const int64_t blk = blockIdx.y >> 1;
     const int parity = blockIdx.y & 1;
     const int64_t v0 = blk * kGramBlock;
@@ -138,13 +157,15 @@ __global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(in
 #pragma unroll
                     for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < TJ; ++j) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
+                        for (int j = 0; j < TJ; ++j)
+                            if (!(DIAG && below_diag<TJ, TI>(i, j))) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < TJ; ++j) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
+                        for (int j = 0; j < TJ; ++j)
+                            if (!(DIAG && below_diag<TJ, TI>(i, j))) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
             }
         }
         for (; rr < nr; ++rr) {
@@ -156,7 +177,8 @@ __global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(in
 #pragma unroll
             for (int i = 0; i < TI; ++i)
 #pragma unroll
-                for (int j = 0; j < TJ; ++j) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
+                for (int j = 0; j < TJ; ++j)
+                    if (!(DIAG && below_diag<TJ, TI>(i, j))) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
         }
         __syncthreads();
     }

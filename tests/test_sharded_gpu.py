@@ -62,11 +62,13 @@ def ordered_sum(parts):
 
 
 def case_step_products_and_updates(world):
-    m, w0, ht0 = conditioned_state()
+    # uneven splits (padded window rows, remapped indices) and an odd K (8-byte push path)
+    V, D, K = 1501, 899, 23
+    m, w0, ht0 = conditioned_state(V, D, K)
     plan = ShardPlan(V, D, world)
     vr = [plan.v_range(g) for g in range(world)]
     dr = [plan.d_range(g) for g in range(world)]
-    engines = make_ranks(m, world)
+    engines = make_ranks(m, world, K)
     on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*vr[g])], ht0[slice(*dr[g])])))
     cfg = P.SolverConfig(rank=K, tile_size=TILE)
     trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
