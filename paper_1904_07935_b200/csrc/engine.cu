@@ -216,8 +216,9 @@ void ensure_plans(plnmf_gpu_engine* e, int64_t tile) {
         e->plan_w = kern::plan_tiled_update(e->v, e->k, tile, true, e->device, e->force_streaming);
     }
     e->plan_h = kern::plan_tiled_update(e->d, e->k, tile, false, e->device, e->force_streaming);
-    if (e->plan_w.streaming) {  // the W update's column-major tile scratch (stream_w_kernel)
-        const int64_t xn = kern::stream_w_scratch_doubles(e->plan_w, tile);
+    if (e->plan_w.streaming || e->plan_h.streaming) {  // column-major tile scratch (stream_w_kernel)
+        const int64_t xn = std::max(e->plan_w.streaming ? kern::stream_w_scratch_doubles(e->plan_w, tile) : 0,
+                                    e->plan_h.streaming ? kern::stream_w_scratch_doubles(e->plan_h, tile) : 0);
         if (xn > e->wscratch_n) {
             e->wscratch = dalloc<double>(e, xn);
             e->wscratch_n = xn;
@@ -284,13 +285,18 @@ void prof_report(plnmf_gpu_engine* e, const char* what, int grid) {
 }
 
 void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
+    bool h_fused = false;
     if (alg == PLNMF_ALGORITHM_TILED) {
         check_tile(cfg, e->k);
         ensure_plans(e, cfg.tile_size);
         long long* prof = prof_buffer(e, e->plan_h.grid);
+        // sharded: the Ht all-gather fused into the streaming update (each finished tile to every rank)
+        h_fused = e->shard && e->world > 1 && e->plan_h.streaming && kern::stream_fuses_push(e->k, cfg.tile_size);
+        plnmf::FusedPush fp;
+        if (h_fused) fp = plnmf::shard::fused_push(e, plnmf::kChanHt, e->h_new);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_h, e->d, e->k, cfg.tile_size, cfg.epsilon, false,
                                           e->ht, e->h_new, e->sm, e->r, nullptr, nullptr, nullptr, nullptr, prof,
-                                          e->qpanel);
+                                          e->qpanel, e->wscratch, h_fused ? &fp : nullptr);
         if (prof) prof_report(e, "H update", e->plan_h.grid);
         std::swap(e->ht, e->h_new);  // ht.swap(ws.h_new), tiled.cpp:213
         e->update_macs += tiled_macs(e->d, e->k, cfg.tile_size, false);
@@ -298,7 +304,7 @@ void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         e->launches += kern::reference_update_h(e->s, e->math, e->d, e->k, cfg.epsilon, e->ht, e->r, e->sm);
         e->update_macs += (uint64_t)e->d * e->k * e->k;
     }
-    if (e->shard) plnmf::shard::push_factor(e, plnmf::kChanHt);  // this rank's new Ht rows to every rank
+    if (e->shard && !h_fused) plnmf::shard::push_factor(e, plnmf::kChanHt);  // this rank's new Ht rows to every rank
 }
 
 // The W update with the reference's norm order (Math::reference_order): column
@@ -347,11 +353,17 @@ void update_w_shard(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorith
     check_tile(cfg, e->k);
     ensure_plans(e, cfg.tile_size);
     const plnmf::WorldXch x = plnmf::shard::next_exchange(e);
+    // the W all-gather fused into the update kernel: each finished tile goes to every rank's
+    // window while the later tiles compute (a separate push kernel when the kernel cannot)
+    const bool fuse = e->world > 1 && kern::stream_fuses_push(e->k, cfg.tile_size);
+    plnmf::FusedPush fp;
+    if (fuse) fp = plnmf::shard::fused_push(e, plnmf::kChanW, e->w_new);
     e->launches += kern::stream_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true, e->w,
-                                       e->w_new, e->q, e->p, e->norms, e->partials, e->counters, &x, e->wscratch);
+                                       e->w_new, e->q, e->p, e->norms, e->partials, e->counters, &x, e->wscratch,
+                                       fuse ? &fp : nullptr);
     std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
     e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);
-    plnmf::shard::push_factor(e, plnmf::kChanW);
+    if (!fuse) plnmf::shard::push_factor(e, plnmf::kChanW);
     e->s_valid = false;
     e->r_valid = false;
 }

@@ -121,6 +121,8 @@ void push_factor(plnmf_gpu_engine* e, PeerChannel c);    // this rank's W (Ht) r
 void reduce_kxk(plnmf_gpu_engine* e, PeerChannel c, double* inout);  // rank-ordered sum of K x K partials
 void reduce_scalar(plnmf_gpu_engine* e, double* inout);              // rank-ordered sum of one double
 WorldXch next_exchange(plnmf_gpu_engine* e);             // norm-exchange arguments of the next W update
+// the all-gather of channel c fused into the kernel that writes out_local (this rank's slice)
+FusedPush fused_push(plnmf_gpu_engine* e, PeerChannel c, const double* out_local);
 void check_error(plnmf_gpu_engine* e);                   // raise a peer timeout recorded on the device
 void close_peers(plnmf_gpu_engine* e);
 }  // namespace shard

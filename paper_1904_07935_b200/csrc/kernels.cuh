@@ -96,10 +96,13 @@ PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize
 // xch (sharded W update, world > 1): every column's sum of squares is also
 // exchanged with the other ranks over peer memory (peer.cuh: world_sum).
 // scratch (W only, stream_w_scratch_doubles): phase 2 on a column-major copy of each tile.
+// push (with xch, world > 1): the finished tiles are also stored into every other rank's
+// window and the channel flag released at the end (requires stream_fuses_push(k, tile)).
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                   const double* add, double* norms, double* partials, unsigned* counters,
-                  const WorldXch* xch = nullptr, double* scratch = nullptr);
+                  const WorldXch* xch = nullptr, double* scratch = nullptr, const FusedPush* push = nullptr);
+bool stream_fuses_push(int64_t k, int64_t tile);
 int64_t stream_w_scratch_doubles(const PhaseBPlan& plan, int64_t tile);
 // init_new_accumulator + phase1_left_contributions into nb (tiled.cpp:28-65).
 int stream_phase_a(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
@@ -114,7 +117,8 @@ int shard_phase3(cudaStream_t s, Math m, int64_t n, int64_t k, int64_t b, int64_
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
-                 long long* prof, double* qpanel, double* stream_scratch = nullptr);
+                 long long* prof, double* qpanel, double* stream_scratch = nullptr,
+                 const FusedPush* push = nullptr);
 
 // Workspace of the grid-wide norm exchange (replicated partials + counters).
 int64_t exchange_partials_doubles(int64_t k, int g);

@@ -90,6 +90,32 @@ __device__ __forceinline__ bool wait_flag(const unsigned* flag, unsigned epoch, 
     return true;
 }
 
+// A collective fused into a producing kernel: the kernel stores each finished
+// piece of its output into every other rank's window as well (dst: this rank's
+// slice there, same layout as the local output), and the last CTA to finish
+// releases the channel's epoch flag in every window (flag[p]).
+struct FusedPush {
+    int world = 1, rank = 0;
+    unsigned epoch = 0;
+    unsigned* done = nullptr;           // zeroed local CTA counter
+    double* dst[kMaxWorld] = {};
+    unsigned* flag[kMaxWorld] = {};
+};
+
+// the end of a kernel that pushed with f: every CTA calls it (all threads)
+__device__ __forceinline__ void fused_push_finish(const FusedPush& f) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // this CTA's peer stores before its count
+        const unsigned prev = atomicAdd(f.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *f.done = 0;
+            __threadfence_system();
+            for (int p = 0; p < f.world; ++p) st_release_sys_u32(f.flag[p], f.epoch);
+        }
+    }
+}
+
 // The world's sum for column t, called by one full warp of every CTA after
 // the rank-local grid exchange has given every CTA the same local sum.  The
 // world's values are added in rank order by every CTA of every rank.

@@ -111,6 +111,22 @@ void reduce_scalar(plnmf_gpu_engine* e, double* inout) {
     e->launches += kern::sum_parts(e->s, reinterpret_cast<const double*>(e->win + e->lay.off_pw), e->world, 1, 1, inout);
 }
 
+FusedPush fused_push(plnmf_gpu_engine* e, PeerChannel c, const double* out_local) {
+    require_connected(e);
+    FusedPush f;
+    f.world = e->world;
+    f.rank = e->rank;
+    f.epoch = ++e->ag_epoch[c];
+    f.done = e->push_done;
+    const size_t off = (size_t)(reinterpret_cast<const char*>(out_local) - e->win);
+    const PeerPtrs flags = flag_slots(e, c);
+    for (int p = 0; p < e->world; ++p) {
+        f.dst[p] = reinterpret_cast<double*>(section(e, p, off));
+        f.flag[p] = static_cast<unsigned*>(flags.p[p]);
+    }
+    return f;
+}
+
 WorldXch next_exchange(plnmf_gpu_engine* e) {
     WorldXch x;
     x.world = e->world;

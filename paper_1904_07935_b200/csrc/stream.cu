@@ -107,6 +107,7 @@ struct StreamArgs {
     WorldXch xch;  // WORLD: the other ranks' windows (sharded engine)
     double* xs;    // stream_w_kernel: per-CTA column-major tile scratch, 3 x tile x ldx doubles per CTA
     int64_t ldx;
+    FusedPush push;  // WORLD: the finished tiles also go to every other rank's window (all-gather)
 };
 
 template <class M, bool NORMALIZE, bool WORLD = false>
@@ -213,7 +214,10 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs 
 // per-element operation order as stream_update_kernel.
 constexpr int kSWarps = kSThreads / kWarp;
 
-template <class M, bool WORLD>
+// NORMALIZE: the W update (every column normalised through the grid exchange); without it
+// the H update.  WORLD (sharded): W's norm exchange spans the ranks, and the finished tiles
+// are pushed into every other rank's window (the factor all-gather fused into the update).
+template <class M, bool NORMALIZE, bool WORLD>
 __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
     __shared__ double red[48];
     // dynamic: phase 3's negated coefficient rows (w x (k - e)); the transposes' per-warp stages
@@ -286,23 +290,26 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
                     }
                     const double val = clamp_floor(p.eps, dsub(dadd(AC[tt * ld + i], AD[tt * ld + i]), s));
                     X[tt * ld + i] = val;
-                    ss = M::madd(ss, val, val);
+                    if (NORMALIZE) ss = M::madd(ss, val, val);
                 }
             }
-            const double blk = block_sum(ss, red);
-            if (tid < kWarp) {
-                const double nrm =
-                    WORLD ? __dsqrt_rn(world_sum(grid_exchange_sum(blk, t, gridDim.x, p.partials, p.counters), t, p.xch))
-                          : grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
-                if (tid == 0) {
-                    red[40] = nrm;
-                    if (blockIdx.x == 0) p.norms[t] = nrm;
+            if (NORMALIZE) {
+                const double blk = block_sum(ss, red);
+                if (tid < kWarp) {
+                    const double nrm =
+                        WORLD ? __dsqrt_rn(world_sum(grid_exchange_sum(blk, t, gridDim.x, p.partials, p.counters), t,
+                                                     p.xch))
+                              : grid_exchange(blk, t, gridDim.x, p.partials, p.counters);
+                    if (tid == 0) {
+                        red[40] = nrm;
+                        if (blockIdx.x == 0) p.norms[t] = nrm;
+                    }
                 }
+                __syncthreads();
+                const double norm = red[40];
+                for (int64_t i = tid; i < nl; i += kSThreads)
+                    X[tt * ld + i] = clamp_floor(p.eps, __ddiv_rn(X[tt * ld + i], norm));  // tiled.cpp:146
             }
-            __syncthreads();
-            const double norm = red[40];
-            for (int64_t i = tid; i < nl; i += kSThreads)
-                X[tt * ld + i] = clamp_floor(p.eps, __ddiv_rn(X[tt * ld + i], norm));  // tiled.cpp:146
         }
         // ---- phase 3 (tiled.cpp:158-174): nb(r, c) += (-coeff(b+j, c)) * new(r, b+j), j ascending,
         // for every c >= e.  One thread per row: the row's w new values (a coalesced column read of X)
@@ -374,19 +381,31 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
             }
         }
         __syncthreads();
-        // ---- the finished tile back to the row-major factor (the same warp-level transpose)
+        // ---- the finished tile back to the row-major factor (the same warp-level transpose);
+        // sharded: also into every other rank's window — the W all-gather fused into the update,
+        // each tile's rows travelling over NVLink while the later tiles compute
         for (int64_t i0 = (int64_t)warp * kWarp; i0 < nl; i0 += (int64_t)kSWarps * kWarp) {
             if (i0 + lane < nl)
                 for (int j = 0; j < w; ++j) st[j * (kWarp + 1) + lane] = X[j * ld + i0 + lane];
             __syncwarp();
             for (int idx = lane; idx < kWarp * w; idx += kWarp) {
                 const int ii = idx / w, j = idx - ii * w;
-                if (i0 + ii < nl) p.nb[(r0 + i0 + ii) * k + b + j] = st[j * (kWarp + 1) + ii];
+                if (i0 + ii < nl) {
+                    const int64_t g = (r0 + i0 + ii) * k + b + j;
+                    const double v = st[j * (kWarp + 1) + ii];
+                    p.nb[g] = v;
+                    if (WORLD) {
+#pragma unroll
+                        for (int q = 0; q < kMaxWorld; ++q)
+                            if (q < p.push.world && q != p.push.rank) p.push.dst[q][g] = v;
+                    }
+                }
             }
             __syncwarp();
         }
         __syncthreads();
     }
+    if (WORLD) fused_push_finish(p.push);
 }
 
 int sm_count(int device) {
@@ -431,10 +450,15 @@ int64_t stream_w_scratch_doubles(const PhaseBPlan& plan, int64_t tile) {
     return (int64_t)plan.grid * 3 * tile * plan.rows_per_cta;
 }
 
+bool stream_fuses_push(int64_t k, int64_t tile) {
+    const size_t w_smem = sizeof(double) * (size_t)std::max<int64_t>(tile * k, (int64_t)kSWarps * tile * (kWarp + 1));
+    return tile <= 32 && w_smem <= 200 * 1024;
+}
+
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                   const double* add, double* norms, double* partials, unsigned* counters, const WorldXch* xch,
-                  double* scratch) {
+                  double* scratch, const FusedPush* push) {
     if (n <= 0 || k <= 0) return 0;
     // phase A: init + phase 1 into `out` (used as the accumulator nb)
     const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
@@ -446,34 +470,41 @@ int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int
     const bool world = xch && xch->world > 1;
     // stream_w_kernel: tiles up to 32 wide; shared memory for the coefficient rows and the stages
     const size_t w_smem = sizeof(double) * (size_t)std::max<int64_t>(tile * k, (int64_t)kSWarps * tile * (kWarp + 1));
-    if (scratch && (tile > 32 || w_smem > 200 * 1024)) scratch = nullptr;
+    if (scratch && !stream_fuses_push(k, tile)) scratch = nullptr;
+    if (push && push->world > 1 && !scratch) throw std::logic_error("stream_update: a fused push needs stream_w_kernel");
     StreamArgs a{n, (int)k, (int)tile, eps, plan.rows_per_cta, old_m, out, coeff, add, norms, partials, counters,
-                 world ? *xch : WorldXch{}, scratch, plan.rows_per_cta};
+                 world ? *xch : WorldXch{}, scratch, plan.rows_per_cta, push ? *push : FusedPush{}};
     const dim3 grid((unsigned)plan.grid), block(kSThreads);
-    if (w_update) {
-        exchange_reset(s, k, plan.grid, partials, counters);
-        void* args[] = {&a};
-        const void* fn;
-        if (scratch)  // column-major tile scratch (stream_w_kernel)
-            fn = world ? ((m == Math::exact) ? (const void*)stream_w_kernel<MathExact, true>
-                                             : (const void*)stream_w_kernel<MathFused, true>)
-                       : ((m == Math::exact) ? (const void*)stream_w_kernel<MathExact, false>
-                                             : (const void*)stream_w_kernel<MathFused, false>);
-        else
-            fn = world ? ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true, true>
-                                             : (const void*)stream_update_kernel<MathFused, true, true>)
-                       : ((m == Math::exact) ? (const void*)stream_update_kernel<MathExact, true>
-                                             : (const void*)stream_update_kernel<MathFused, true>);
+    const bool pushing = push && push->world > 1;
+    const size_t smem = scratch ? w_smem : 0;
+    void* args[] = {&a};
+    auto launch = [&](const void* fn, bool cooperative) {
+        // stream_w_kernel: the tile's coefficient rows for phase 3 in dynamic shared memory
+        if (smem > 48 * 1024) PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // a plan with fewer CTAs than SMs (ranks sharing one GPU) is co-resident with
         // the other ranks' kernels only under a plain launch
-        // stream_w_kernel: the tile's coefficient rows for phase 3 in dynamic shared memory
-        const size_t smem = scratch ? w_smem : 0;
-        if (smem > 48 * 1024) PLNMF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (plan.cooperative)
-            PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s));
+        if (cooperative) PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s));
+        else PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, smem, s));
+    };
+    const bool ex = m == Math::exact;
+    if (w_update) {
+        exchange_reset(s, k, plan.grid, partials, counters);
+        const void* fn;
+        if (scratch)  // column-major tile scratch (stream_w_kernel)
+            fn = world ? (ex ? (const void*)stream_w_kernel<MathExact, true, true> : (const void*)stream_w_kernel<MathFused, true, true>)
+                       : (ex ? (const void*)stream_w_kernel<MathExact, true, false> : (const void*)stream_w_kernel<MathFused, true, false>);
         else
-            PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, grid, block, args, smem, s));
-    } else if (m == Math::exact) {
+            fn = world ? (ex ? (const void*)stream_update_kernel<MathExact, true, true>
+                             : (const void*)stream_update_kernel<MathFused, true, true>)
+                       : (ex ? (const void*)stream_update_kernel<MathExact, true> : (const void*)stream_update_kernel<MathFused, true>);
+        launch(fn, plan.cooperative);
+    } else if (scratch) {
+        const void* fn = pushing ? (ex ? (const void*)stream_w_kernel<MathExact, false, true>
+                                       : (const void*)stream_w_kernel<MathFused, false, true>)
+                                 : (ex ? (const void*)stream_w_kernel<MathExact, false, false>
+                                       : (const void*)stream_w_kernel<MathFused, false, false>);
+        launch(fn, false);
+    } else if (ex) {
         stream_update_kernel<MathExact, false><<<grid, block, 0, s>>>(a);
     } else {
         stream_update_kernel<MathFused, false><<<grid, block, 0, s>>>(a);

@@ -123,6 +123,9 @@ def case_iterate_matches_single_engine(world):
     f1 = single.get_factors()
 
     engines = make_ranks(m, world)
+    if world == 3:  # H on the streaming plan too: the Ht all-gather fused into that kernel
+        for e in engines:
+            e.force_streaming(True)
     on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*plan.v_range(g))],
                                                               ht0[slice(*plan.d_range(g))])))
     trs = on_ranks(engines, lambda e, g: e.iterate(cfg, P.Algorithm.tiled))
