@@ -35,6 +35,7 @@ void release(plnmf_gpu_engine* e) {
     for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
     if (e->fork) cudaEventDestroy(e->fork);
     if (e->join_r) cudaEventDestroy(e->join_r);
+    if (e->err_done) cudaEventDestroy(e->err_done);
     if (e->join) cudaEventDestroy(e->join);
     if (e->s) cudaStreamDestroy(e->s);
     if (e->s2) cudaStreamDestroy(e->s2);
@@ -61,6 +62,7 @@ void setup_common(plnmf_gpu_engine* e, int device, int64_t rank) {
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join_r, cudaEventDisableTiming));
+    PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->err_done, cudaEventDisableTiming));
 }
 
 // The workspace (UpdateWorkspace, proj/include/plnmf/workspace.hpp:15-55).  A
@@ -432,7 +434,19 @@ ErrorReport direct_error(plnmf_gpu_engine* e) {
 // gram(W) is done, next to the error reductions and the host round trip
 // (measured: 1.83 ms/iteration vs 1.87 with R beside the Gram and 1.85 with R
 // after the reductions).
+// evaluate_error in two halves: launch (the kernels and the asynchronous readback of the
+// 3-double report, completion recorded in `done`) and finish (read it after `done`; the
+// direct fallback below 1e-6).  iterate() queues work between the two.
+void evaluate_error_launch(plnmf_gpu_engine* e, bool ahead_r, cudaEvent_t done);
+ErrorReport evaluate_error_finish(plnmf_gpu_engine* e, cudaEvent_t done);
+
 ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
+    cudaEvent_t done = e->err_done;
+    evaluate_error_launch(e, ahead_r, done);
+    return evaluate_error_finish(e, done);
+}
+
+void evaluate_error_launch(plnmf_gpu_engine* e, bool ahead_r, cudaEvent_t done) {
     if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_gram: zero input norm");
     if (!(e->a2 == e->a2)) throw std::invalid_argument("sharded engine: ||A||^2 not set (plnmf_gpu_shard_set_norm_sq)");
     e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
@@ -456,7 +470,11 @@ ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
     }
     e->launches += kern::error_finalize(e->s, e->a2, e->scalars + 0, e->scalars + 1, e->scalars + 2);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 2, e->scalars + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->s));
-    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+    PLNMF_CUDA_CHECK(cudaEventRecord(done, e->s));
+}
+
+ErrorReport evaluate_error_finish(plnmf_gpu_engine* e, cudaEvent_t done) {
+    PLNMF_CUDA_CHECK(cudaEventSynchronize(done));
     if (e->shard) plnmf::shard::check_error(e);
     ErrorReport rep;
     rep.frob = e->host_scalars[2];
@@ -550,44 +568,83 @@ void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, 
     double prev = initial;
     int64_t n_rec = 0;
 
-    for (int64_t it = 1; it <= cfg.max_iters; ++it) {
-        PLNMF_CUDA_CHECK(cudaEventRecord(ev[0], e->s));
+    // Speculation (tiled updates, single engine): while the host waits for an error report,
+    // the next iteration's precompute_h and update_h are already queued behind it, so the
+    // GPU does not idle through the readback and the stop-rule check.  update_h writes the
+    // other Ht buffer, so stopping undoes it by swapping the buffers back; everything else it
+    // touches (R consumed, S unchanged) stays valid for the final factors.
+    const bool can_spec = tiled && !e->shard;
+    bool spec = false;  // this iteration's precompute_h + update_h were queued by the previous one
+    int set = 0;        // event set of this iteration (the speculative half records into the other)
+    auto evs = [&](int st, int i) { return event_at(e, (size_t)(8 + 8 * st + i)); };
+    auto queue_h_half = [&](int st) {
+        PLNMF_CUDA_CHECK(cudaEventRecord(evs(st, 0), e->s));
         precompute_h(e);
-        PLNMF_CUDA_CHECK(cudaEventRecord(ev[1], e->s));
+        PLNMF_CUDA_CHECK(cudaEventRecord(evs(st, 1), e->s));
         update_h(e, cfg, alg);
-        PLNMF_CUDA_CHECK(cudaEventRecord(ev[2], e->s));
+        PLNMF_CUDA_CHECK(cudaEventRecord(evs(st, 2), e->s));
+    };
+    auto undo_h_half = [&] {
+        std::swap(e->ht, e->h_new);  // back to the Ht the final W was computed from
+        e->update_macs -= tiled_macs(e->d, e->k, cfg.tile_size, false);
+        e->r_valid = false;
+    };
+
+    for (int64_t it = 1; it <= cfg.max_iters; ++it) {
+        if (!spec) queue_h_half(set);
+        spec = false;
         precompute_w(e);
-        PLNMF_CUDA_CHECK(cudaEventRecord(ev[3], e->s));
+        PLNMF_CUDA_CHECK(cudaEventRecord(evs(set, 3), e->s));
         update_w(e, cfg, alg);
-        PLNMF_CUDA_CHECK(cudaEventRecord(ev[4], e->s));
+        PLNMF_CUDA_CHECK(cudaEventRecord(evs(set, 4), e->s));
         const bool eval = it % cfg.error_every == 0;
-        // The error evaluation is queued right behind the W update (its own readback is the
-        // iteration's one host synchronisation); the phase times are read after it.
-        if (!eval) PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
         plnmf_phase_times ph{};
         auto phase_times = [&] {
-            ph.precompute_h = elapsed_s(ev[0], ev[1]);
-            ph.precompute_w = elapsed_s(ev[2], ev[3]);
+            ph.precompute_h = elapsed_s(evs(set, 0), evs(set, 1));
+            ph.precompute_w = elapsed_s(evs(set, 2), evs(set, 3));
             if (tiled) {
                 // one fused look-ahead kernel per update (init, phases 1-3, normalisation)
-                ph.phase2 = elapsed_s(ev[1], ev[2]) + elapsed_s(ev[3], ev[4]);
+                ph.phase2 = elapsed_s(evs(set, 1), evs(set, 2)) + elapsed_s(evs(set, 3), evs(set, 4));
             } else {
-                ph.update_h = elapsed_s(ev[1], ev[2]);
-                ph.update_w = elapsed_s(ev[3], ev[4]);
+                ph.update_h = elapsed_s(evs(set, 1), evs(set, 2));
+                ph.update_w = elapsed_s(evs(set, 3), evs(set, 4));
             }
         };
         if (eval) {
             // next iteration's R = A^T W computed ahead (unused if the loop stops)
-            const ErrorReport rep = evaluate_error(e, e->sparse && !e->shard && it < cfg.max_iters);
-            PLNMF_CUDA_CHECK(cudaEventRecord(ev[5], e->s));
-            PLNMF_CUDA_CHECK(cudaEventSynchronize(ev[5]));
+            evaluate_error_launch(e, e->sparse && !e->shard && it < cfg.max_iters, e->err_done);
+            PLNMF_CUDA_CHECK(cudaEventRecord(evs(set, 5), e->s));
+            if (can_spec && it < cfg.max_iters) {
+                queue_h_half(set ^ 1);
+                spec = true;
+            }
+            PLNMF_CUDA_CHECK(cudaEventSynchronize(evs(set, 5)));
+            ErrorReport rep;
+            {
+                ErrorReport r0;
+                r0.frob = e->host_scalars[2];
+                r0.rel = e->host_scalars[3];
+                r0.cancellation = e->host_scalars[4] != 0.0;
+                if (e->shard) plnmf::shard::check_error(e);
+                if (r0.rel < 1e-6) {  // the direct fallback reads Ht: not with the speculative one
+                    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+                    if (spec) undo_h_half();
+                    spec = false;
+                    r0 = direct_error(e);
+                }
+                rep = r0;
+            }
             phase_times();
-            // the evaluation's own time (from the end of the W update to its readback), not the
-            // update work the host call waited behind
-            ph.error_eval = elapsed_s(ev[4], ev[5]);
+            // the evaluation's own time (from the end of the W update to its readback)
+            ph.error_eval = elapsed_s(evs(set, 4), evs(set, 5));
             add_times(totals, ph);
-            if (!std::isfinite(rep.rel))
+            if (!std::isfinite(rep.rel)) {
+                if (spec) {
+                    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+                    undo_h_half();
+                }
                 throw plnmf::NonFinite("iterate: objective became non-finite at iteration " + std::to_string(it));
+            }
             if (trace && trace->records) {
                 plnmf_trace_record& rec = trace->records[n_rec];
                 rec.iteration = it;
@@ -598,14 +655,22 @@ void iterate(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg, 
             ++n_rec;
             if (prev > 0.0 && std::fabs(prev - rep.rel) / prev < cfg.rel_tol) {
                 prev = rep.rel;
+                if (spec) {
+                    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
+                    undo_h_half();
+                    spec = false;
+                }
                 break;
             }
             prev = rep.rel;
         } else {
+            PLNMF_CUDA_CHECK(cudaEventSynchronize(evs(set, 4)));
             phase_times();
             add_times(totals, ph);
         }
+        if (spec) set ^= 1;
     }
+    PLNMF_CUDA_CHECK(cudaStreamSynchronize(e->s));
     if (trace) {
         trace->initial_error = initial;
         trace->n_records = n_rec;
