@@ -124,6 +124,12 @@ def cpu_model():
     return "unknown"
 
 
+# BENCH_DIST_BACKEND=gloo (a test hook): the ranks' bootstrap and host-side reductions over gloo,
+# and ranks may share GPUs (LOCAL_RANK modulo the visible devices) — the launch path of N GPUs
+# exercised on one (the ranks' contexts then time-slice the GPU: correct but not a measurement).
+DIST_BACKEND = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
 def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -131,19 +137,29 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group(DIST_BACKEND)
         return rank, world, local, dist
     return rank, world, local, None
+
+
+def _reduce(dist, local, x: float, op) -> float:
+    import torch
+    dev = f"cuda:{local}" if DIST_BACKEND == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t.item())
 
 
 def allmax(dist, local, x: float) -> float:
     if dist is None:
         return x
-    import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _reduce(dist, local, x, dist.ReduceOp.MAX)
 
 
 def barrier(dist):
@@ -558,10 +574,7 @@ def time_reference_c5(steps):
 def allsum(dist, local, x: float) -> float:
     if dist is None:
         return x
-    import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t)
-    return float(t.item())
+    return _reduce(dist, local, x, dist.ReduceOp.SUM)
 
 
 def main():
