@@ -207,6 +207,11 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
         // persistent + grid-synchronised: exactly one resident CTA per SM with
         // one SM's rows (one row per chain thread); otherwise the streaming path
         v = rpc <= 8 * 32 ? pick(rpc) : -1;
+        // neither the operands nor the coefficient panel staged (plan 2): at large K the look-ahead
+        // re-reads the panel from global for every row and the streaming kernel wins (measured,
+        // tools/tile_plans.py: TDT2 K=480, T=20-32: 8.0-10.0 ms vs 5.2-5.9 ms per W update; at
+        // 20News K=240, T=24 the look-ahead still wins, 1.57 vs 1.71 ms)
+        if (v == 2 && k > 320) v = -1;
         if (v < 0) return plan_stream_update(n, k, tile, normalize, device);
         plan.grid = sms;
         plan.cooperative = true;

@@ -82,8 +82,8 @@ def test_c3_tdt2_k480(gpu):
         eng.update_h(c, A.tiled)
         eng.precompute_w_products()
         eng.update_w(c, A.tiled)
-        if tile == 22:
-            assert eng.stats()["w_plan"] == 2  # the unstaged persistent W kernel
+        if tile == 22:  # K=480, 249 rows per SM: the panel does not fit, the streaming W kernel
+            assert eng.stats()["w_plan"] == 3
         rep = eng.evaluate_error()
         got = eng.get_factors()
         w1, ht1 = ses.one_iteration(w, ht, tile=tile)

@@ -84,12 +84,14 @@ def test_gram_and_spmm_20news_shape_bitwise(gpu):
     assert bits_equal(eng.get_product("r"), R.spmm(m.cols, m.rows, trp, tci, tval, f.w))
 
 
-@pytest.mark.parametrize("tile", [16, 22])
-def test_tiled_updates_20news_scale(gpu, tile):
+@pytest.mark.parametrize("tile,w_plan", [(16, 0), (20, 1), (24, 2)])
+def test_tiled_updates_20news_scale(gpu, tile, w_plan):
     """The bench shape (C2, K=240): 77 H rows / 178 W rows per SM, so the
     staged look-ahead GEMM (lookahead_gemm_private) and the latency-ordered W
     chain run exactly as in bench.py.  H bitwise; W (norm reduction order
-    only) to 1e-12 from the oracle's own H-updated state."""
+    only) to 1e-12 from the oracle's own H-updated state.  The tile sizes
+    reach the three look-ahead W plans (operands + panel staged, panel only,
+    neither)."""
     k = 240
     m, eng, f = make(**NEWS20, k=k)
     eng.precompute_h_products()
@@ -101,6 +103,7 @@ def test_tiled_updates_20news_scale(gpu, tile):
     eng.precompute_w_products()
     p, q = eng.get_product("p"), eng.get_product("q")
     eng.update_w(cfg, A.tiled)
+    assert eng.stats()["w_plan"] == w_plan
     w1, norms = R.update_tiled(f.w, q, p, tile, is_w=True)
     w_eng = eng.get_factors().w
     assert rel_max(w1, w_eng) <= 1e-12
