@@ -63,12 +63,15 @@ typedef enum plnmf_math {
      * With it, iterate() trajectories are bit-identical to the reference's.
      * Column-stepped and slow (serial chains): not the production path. */
     PLNMF_MATH_REFERENCE_ORDER = 2,
-    /* EXACT, except that a DENSE input's products P = A Ht and R = A^T W
-     * (hals.cpp:29,43) run on the tensor cores: each fp64 operand row is
-     * scaled by a power of two and cut into six 8-bit digits, the 21 digit
-     * products that matter are exact u8 x u8 tcgen05.mma GEMMs with int32
-     * accumulators in TMEM, combined in fp64 (the Ozaki scheme; csrc/ozaki.cu).
-     * Relative error ~1e-14 per entry; not the reference's summation order. */
+    /* EXACT, except that (a) a DENSE input's products P = A Ht and R = A^T W
+     * (hals.cpp:29,43) and (b) the inter-tile phase A of a streaming tiled
+     * update — init_new_accumulator + phase1_left_contributions for every column
+     * at once (tiled.cpp:28-65), as init - old * U — run on the tensor cores:
+     * each fp64 operand row is scaled by a power of two and cut into six 8-bit
+     * digits, the 21 digit products that matter are exact u8 x u8 tcgen05.mma
+     * GEMMs with int32 accumulators in TMEM, combined in fp64 (the Ozaki scheme;
+     * csrc/ozaki.cu).  Error bounded by n 2^-46 times the operand scales; not the
+     * reference's summation order. */
     PLNMF_MATH_TENSOR = 3
 } plnmf_math;
 

@@ -148,6 +148,17 @@ void tensor_at_w(plnmf_gpu_engine* e) {
     e->launches += kern::ozaki_gemm(e->s, e->d, e->k, e->v, e->dig_ar, e->sc_ar, e->dig_b, e->sc_b, e->oz_part, e->r);
 }
 
+// Math::tensor workspace of the streaming updates' phase A (kern::tensor_phase_a), or null
+void* tensor_phase_a_ws(plnmf_gpu_engine* e, const kern::PhaseBPlan& plan) {
+    if (!e->tensor || !plan.streaming) return nullptr;
+    const int64_t bytes = kern::tensor_phase_a_bytes(std::max(e->v, e->d), e->k);
+    if (bytes > e->tensor_ws_bytes) {
+        e->tensor_ws = dalloc<char>(e, bytes);
+        e->tensor_ws_bytes = bytes;
+    }
+    return e->tensor_ws;
+}
+
 // ---- products ------------------------------------------------------------------------
 // rows of the gathered operand of R = A^T W / P = A Ht (a shard's padded full factor)
 int64_t operand_rows_w(const plnmf_gpu_engine* e) { return e->shard ? e->world * e->vcap : e->v; }
@@ -298,7 +309,8 @@ void update_h(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         if (h_fused) fp = plnmf::shard::fused_push(e, plnmf::kChanHt, e->h_new);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_h, e->d, e->k, cfg.tile_size, cfg.epsilon, false,
                                           e->ht, e->h_new, e->sm, e->r, nullptr, nullptr, nullptr, nullptr, prof,
-                                          e->qpanel, e->wscratch, h_fused ? &fp : nullptr);
+                                          e->qpanel, e->wscratch, h_fused ? &fp : nullptr,
+                                          tensor_phase_a_ws(e, e->plan_h));
         if (prof) prof_report(e, "H update", e->plan_h.grid);
         std::swap(e->ht, e->h_new);  // ht.swap(ws.h_new), tiled.cpp:213
         e->update_macs += tiled_macs(e->d, e->k, cfg.tile_size, false);
@@ -379,7 +391,7 @@ void update_w(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg)
         long long* prof = prof_buffer(e, e->plan_w.grid);
         e->launches += kern::tiled_update(e->s, e->math, e->plan_w, e->v, e->k, cfg.tile_size, cfg.epsilon, true,
                                           e->w, e->w_new, e->q, e->p, e->norms, e->partials, e->counters, e->totals,
-                                          prof, e->qpanel, e->wscratch);
+                                          prof, e->qpanel, e->wscratch, nullptr, tensor_phase_a_ws(e, e->plan_w));
         if (prof) prof_report(e, "W update", e->plan_w.grid);
         std::swap(e->w, e->w_new);  // w.swap(ws.w_new), tiled.cpp:192
         e->update_macs += tiled_macs(e->v, e->k, cfg.tile_size, true);
@@ -1008,7 +1020,9 @@ plnmf_status plnmf_gpu_set_math(plnmf_gpu_engine* e, plnmf_math math) {
             throw std::invalid_argument("plnmf_gpu_set_math: a sharded engine runs Math::exact or Math::fused");
         e->math = math == PLNMF_MATH_FUSED ? Math::fused : Math::exact;
         e->ref_order = math == PLNMF_MATH_REFERENCE_ORDER;
-        e->tensor = math == PLNMF_MATH_TENSOR && !e->sparse;  // sparse inputs have no dense GEMM
+        // Math::tensor: the dense-A products (dense inputs) and phase A of streaming tiled
+        // updates (any input) on the tensor cores
+        e->tensor = math == PLNMF_MATH_TENSOR;
         e->s_valid = false;
         e->r_valid = false;
     });

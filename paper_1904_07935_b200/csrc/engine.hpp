@@ -67,6 +67,8 @@ struct plnmf_gpu_engine {
     long long* prof = nullptr;        // PLNMF_PROFILE=1: phase-B section cycle counters
     int64_t prof_n = 0;
     double* wscratch = nullptr;       // streaming W update: column-major tile scratch (stream.cu)
+    char* tensor_ws = nullptr;        // Math::tensor: phase A of the streaming updates (ozaki.cu)
+    int64_t tensor_ws_bytes = 0;
     int64_t wscratch_n = 0;
     double* qpanel = nullptr;         // coeff column panels of the tiled updates
     int64_t qpanel_n = 0;

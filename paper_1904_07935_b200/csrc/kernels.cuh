@@ -68,6 +68,14 @@ int64_t ozaki_partial_doubles(int64_t m, int64_t n, int64_t kdim);
 int ozaki_gemm(cudaStream_t s, int64_t m, int64_t n, int64_t kdim, const uint8_t* a_digits, const double* sa,
                const uint8_t* b_digits, const double* sb, double* part, double* out);
 
+// Math::tensor phase A of the streaming tiled update: init_new_accumulator +
+// phase1_left_contributions (tiled.cpp:28-65) for every column at once as
+// init - old * U (U: phase 1's coefficients), the product an Ozaki tcgen05 GEMM.
+// ws: tensor_phase_a_bytes(n, k) bytes.
+int64_t tensor_phase_a_bytes(int64_t n, int64_t k);
+int tensor_phase_a(cudaStream_t s, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
+                   const double* coeff, double* nb, void* ws);
+
 // ---- tiled (PL-NMF) update, proj/src/tiled.cpp:176-214 --------------------------
 struct PhaseBPlan {
     int grid = 0;            // CTAs
@@ -98,10 +106,12 @@ PhaseBPlan plan_stream_update(int64_t n, int64_t k, int64_t tile, bool normalize
 // scratch (W only, stream_w_scratch_doubles): phase 2 on a column-major copy of each tile.
 // push (with xch, world > 1): the finished tiles are also stored into every other rank's
 // window and the channel flag released at the end (requires stream_fuses_push(k, tile)).
+// tensor_ws (Math::tensor): phase A on the tensor cores (tensor_phase_a).
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                   const double* add, double* norms, double* partials, unsigned* counters,
-                  const WorldXch* xch = nullptr, double* scratch = nullptr, const FusedPush* push = nullptr);
+                  const WorldXch* xch = nullptr, double* scratch = nullptr, const FusedPush* push = nullptr,
+                  void* tensor_ws = nullptr);
 bool stream_fuses_push(int64_t k, int64_t tile);
 int64_t stream_w_scratch_doubles(const PhaseBPlan& plan, int64_t tile);
 // init_new_accumulator + phase1_left_contributions into nb (tiled.cpp:28-65).
@@ -118,7 +128,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
                  long long* prof, double* qpanel, double* stream_scratch = nullptr,
-                 const FusedPush* push = nullptr);
+                 const FusedPush* push = nullptr, void* tensor_ws = nullptr);
 
 // Workspace of the grid-wide norm exchange (replicated partials + counters).
 int64_t exchange_partials_doubles(int64_t k, int g);

@@ -316,9 +316,65 @@ __global__ void split_sum_kernel(int64_t mn, int splits, const double* __restric
     out[i] = s;
 }
 
+// U(kk, c) = coeff(kk, c) for kk in the tiles after c's (kk >= e(c)), else 0: phase 1's
+// coefficients (tiled.cpp:52-65) as one matrix
+__global__ void phase1_coeff_kernel(int64_t k, int64_t tile, const double* __restrict__ coeff, double* __restrict__ u) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k * k) return;
+    const int64_t kk = i / k, c = i % k;
+    const int64_t e = ((c / tile) + 1) * tile;
+    u[i] = kk >= e ? coeff[i] : 0.0;
+}
+
+// nb = init - nb (nb holds old * U on entry): init = old * coeff(c, c) for W (tiled.cpp:44), old for H
+__global__ void phase_a_combine_kernel(int64_t n, int64_t k, int use_diag, const double* __restrict__ old_m,
+                                       const double* __restrict__ coeff, double* __restrict__ nb) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * k) return;
+    const int64_t c = i % k;
+    const double init = use_diag ? __dmul_rn(old_m[i], coeff[c * k + c]) : old_m[i];
+    nb[i] = __dsub_rn(init, nb[i]);
+}
+
 }  // namespace ozk
 
 namespace kern {
+
+int64_t tensor_phase_a_bytes(int64_t n, int64_t k) {
+    const int nt = ozaki_nt(k);
+    auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+    return al(sizeof(double) * k * k) + al(ozaki_digit_bytes(n, k, ozk::kMT)) + al(sizeof(double) * n) +
+           al(ozaki_digit_bytes(k, k, nt)) + al(sizeof(double) * k) + al(sizeof(double) * ozaki_partial_doubles(n, k, k));
+}
+
+int tensor_phase_a(cudaStream_t s, int64_t n, int64_t k, int64_t tile, bool use_diag, const double* old_m,
+                   const double* coeff, double* nb, void* ws) {
+    if (n <= 0 || k <= 0) return 0;
+    const int nt = ozaki_nt(k);
+    auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+    char* p = static_cast<char*>(ws);
+    double* u = reinterpret_cast<double*>(p);
+    p += al(sizeof(double) * k * k);
+    uint8_t* dl = reinterpret_cast<uint8_t*>(p);
+    p += al(ozaki_digit_bytes(n, k, ozk::kMT));
+    double* sl = reinterpret_cast<double*>(p);
+    p += al(sizeof(double) * n);
+    uint8_t* dr = reinterpret_cast<uint8_t*>(p);
+    p += al(ozaki_digit_bytes(k, k, nt));
+    double* sr = reinterpret_cast<double*>(p);
+    p += al(sizeof(double) * k);
+    double* part = reinterpret_cast<double*>(p);
+    int launches = 0;
+    ozk::phase1_coeff_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, s>>>(k, tile, coeff, u);
+    ++launches;
+    // left = old (n x k rows), right rows = the columns c of U: element (c, kk) at u[kk * k + c]
+    launches += ozaki_slice(s, n, k, old_m, k, false, ozk::kMT, sl, dl);
+    launches += ozaki_slice(s, k, k, u, k, true, nt, sr, dr);
+    launches += ozaki_gemm(s, n, k, k, dl, sl, dr, sr, part, nb);  // nb := old * U
+    ozk::phase_a_combine_kernel<<<(unsigned)((n * k + 255) / 256), 256, 0, s>>>(n, k, use_diag ? 1 : 0, old_m, coeff, nb);
+    PLNMF_CUDA_CHECK(cudaGetLastError());
+    return launches + 1;
+}
 
 int64_t ozaki_digit_bytes(int64_t rows, int64_t cols, int rt) {
     const int64_t rp = (rows + rt - 1) / rt * rt, nks = (cols + ozk::kKStep - 1) / ozk::kKStep;

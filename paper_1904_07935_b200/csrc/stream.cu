@@ -458,15 +458,20 @@ bool stream_fuses_push(int64_t k, int64_t tile) {
 int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                   double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                   const double* add, double* norms, double* partials, unsigned* counters, const WorldXch* xch,
-                  double* scratch, const FusedPush* push) {
+                  double* scratch, const FusedPush* push, void* tensor_ws) {
     if (n <= 0 || k <= 0) return 0;
     // phase A: init + phase 1 into `out` (used as the accumulator nb)
-    const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
-    if (m == Math::exact)
-        stream_phase_a_kernel<MathExact><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
-    else
-        stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
-    PLNMF_CUDA_CHECK(cudaGetLastError());
+    int launches = 2;
+    if (tensor_ws) {
+        launches += tensor_phase_a(s, n, k, tile, w_update, old_m, coeff, out, tensor_ws) - 1;
+    } else {
+        const dim3 ga((unsigned)((k + kTileCols - 1) / kTileCols), (unsigned)((n + kTileRows - 1) / kTileRows));
+        if (m == Math::exact)
+            stream_phase_a_kernel<MathExact><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
+        else
+            stream_phase_a_kernel<MathFused><<<ga, kPhaseAThreads, 0, s>>>(n, (int)k, (int)tile, w_update, old_m, coeff, out);
+        PLNMF_CUDA_CHECK(cudaGetLastError());
+    }
     const bool world = xch && xch->world > 1;
     // stream_w_kernel: tiles up to 32 wide; shared memory for the coefficient rows and the stages
     const size_t w_smem = sizeof(double) * (size_t)std::max<int64_t>(tile * k, (int64_t)kSWarps * tile * (kWarp + 1));
@@ -510,7 +515,7 @@ int stream_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int
         stream_update_kernel<MathFused, false><<<grid, block, 0, s>>>(a);
     }
     PLNMF_CUDA_CHECK(cudaGetLastError());
-    return 2;
+    return launches;
 }
 
 }  // namespace kern

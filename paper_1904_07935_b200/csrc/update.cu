@@ -267,11 +267,12 @@ int64_t qpanel_doubles(int64_t k, int64_t tile) {
 int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int64_t k, int64_t tile,
                  double eps, bool w_update, const double* old_m, double* out, const double* coeff,
                  const double* add, double* norms, double* partials, unsigned* counters, double* totals,
-                 long long* prof, double* qpanel, double* stream_scratch, const FusedPush* push) {
+                 long long* prof, double* qpanel, double* stream_scratch, const FusedPush* push,
+                 void* tensor_ws) {
     if (n <= 0 || k <= 0) return 0;
     if (plan.streaming)
         return stream_update(s, m, plan, n, k, tile, eps, w_update, old_m, out, coeff, add, norms, partials,
-                             counters, nullptr, stream_scratch, push);
+                             counters, nullptr, stream_scratch, push, tensor_ws);
     if (push && push->world > 1) throw std::logic_error("tiled_update: a fused push needs the streaming plan");
     LookArgs a{n, (int)k, (int)tile, eps, w_update ? 1 : 0, (int)plan.rows_per_cta, old_m, out, coeff, add,
                norms, partials, counters, totals, prof, knob("PLNMF_NO_OVERLAP") ? 0 : knob("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1,

@@ -65,3 +65,32 @@ def test_tensor_one_step_from_a_converging_state(gpu):
     (ee, fe), (et, ft) = out[P.Math.exact], out[P.Math.tensor]
     assert abs(et - ee) <= 1e-12 * ee
     assert rel_max(fe.ht, ft.ht) <= 1e-10 and rel_max(fe.w, ft.w) <= 1e-10
+
+
+@pytest.mark.parametrize("k,tile", [(24, 5), (40, 16), (33, 32)])
+def test_tensor_phase_a_of_streaming_updates(gpu, k, tile):
+    """Math.tensor on a sparse input: the streaming tiled updates' phase A (init +
+    phase 1 for every column, tiled.cpp:28-65) as one Ozaki tcgen05 GEMM.  One
+    iteration from a converging state against the exact path: factors to 1e-9
+    (the fp64 chaos envelope the reference's own two paths define is 1e-3), the
+    error to 1e-11."""
+    m = P.synth_csr(1500, 900, 0.02, 9)
+    eng = P.Engine(P.InputMatrix(m), k)
+    eng.force_streaming(True)
+    cfg = P.SolverConfig(rank=k, max_iters=8, rel_tol=0.0, tile_size=tile)
+    eng.init_factors(cfg)
+    eng.iterate(cfg, P.Algorithm.tiled)
+    state = eng.get_factors()
+    out = {}
+    for math in (P.Math.exact, P.Math.tensor):
+        eng.set_math(math)
+        eng.set_factors(state)
+        eng.precompute_h_products()
+        eng.update_h(cfg, P.Algorithm.tiled)
+        eng.precompute_w_products()
+        eng.update_w(cfg, P.Algorithm.tiled)
+        out[math] = (eng.evaluate_error().relative, eng.get_factors())
+    (ee, fe), (et, ft) = out[P.Math.exact], out[P.Math.tensor]
+    assert rel_max(fe.ht, ft.ht) <= 1e-9 and rel_max(fe.w, ft.w) <= 1e-9
+    assert abs(et - ee) <= 1e-11 * ee
+    assert not bits_equal(fe.w, ft.w)  # the tensor path really ran (a different summation)
