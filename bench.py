@@ -539,11 +539,24 @@ def c5_arm(args):
             "gpu_launches": launches, "clocks": clk.summary(), "phase_ms_per_step": phases,
             "setup_s": setup_s, "nnz_per_rank": nnz_local,
             "parallelism": f"sharded x{world}",
+            "workload_note": "N = 1 runs configs[1] (C2, the metric's config); N > 1 runs configs[4] (C5, the "
+                             "config that shards). The 1-GPU point of THIS workload is `bench.py --workload c5`",
+            "one_gpu_same_workload": c5_one_gpu_reference(),
         }
         print(json.dumps(line), flush=True)
     eng.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def c5_one_gpu_reference():
+    """The committed 1-GPU measurement of the C5 workload (bench.py --workload c5 on a B200)."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r2_bench_c5_1gpu.json").read_text())
+        return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                "source": "profiles/r2_bench_c5_1gpu.json (bench.py --workload c5, one B200)"}
+    except Exception:
+        return None
 
 
 def time_reference_c5(steps):
