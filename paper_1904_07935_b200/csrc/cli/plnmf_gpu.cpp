@@ -8,7 +8,7 @@
 //                         [--algorithm fast-hals|pl-nmf] [--tile auto|scan|gpu|N]
 //                         [--max-iters N] [--tol x] [--epsilon x] [--seed s]
 //                         [--error-every n] [--output path] [--format json|csv-trace]
-//                         [--device i] [--math exact|fused|reference-order] [--threads n]
+//                         [--device i] [--math exact|fused|reference-order|tensor] [--threads n]
 //   plnmf-gpu sweep-tiles (as factorize) [--grid 1,2,4,...]
 //   plnmf-gpu compare     (as factorize): fast-hals and pl-nmf in lockstep on the GPU
 //   plnmf-gpu model       --k K [--v V --d D | --input A.mtx]
@@ -114,7 +114,11 @@ std::unique_ptr<Input> open_input(const Options& o) {
     else if (o.math == "reference-order") {
         check(plnmf_gpu_set_math(in->e, PLNMF_MATH_REFERENCE_ORDER));
         check(plnmf_gpu_set_reference_threads(in->e, o.threads > 0 ? o.threads : 1));
-    } else if (o.math != "exact") throw std::invalid_argument("--math must be exact, fused or reference-order");
+    } else if (o.math == "tensor") {
+        check(plnmf_gpu_set_math(in->e, PLNMF_MATH_TENSOR));
+    } else if (o.math != "exact") {
+        throw std::invalid_argument("--math must be exact, fused, reference-order or tensor");
+    }
     if (o.k > std::min(in->rows, in->cols))
         std::cerr << "warning: K = " << o.k << " exceeds min(V, D) = " << std::min(in->rows, in->cols) << "\n";
     return in;
