@@ -210,8 +210,10 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_update_kernel(StreamArgs 
 // overwritten in place by the new values: exactly the operands the reference
 // reads), the accumulators into AC and the additive term into AD, all
 // column-major, so every phase-2 load is a coalesced column read; the finished
-// tile is copied back to the row-major factor before phase 3.  Same
-// per-element operation order as stream_update_kernel.
+// tile is copied back to the row-major factor.  Phase 3 runs as a look-ahead:
+// only the next tile's accumulators are built (their phase-A values plus every
+// finished tile's terms, in tile order), so the far columns are read but never
+// rewritten.  Same per-element operation order as stream_update_kernel.
 constexpr int kSWarps = kSThreads / kWarp;
 
 // NORMALIZE: the W update (every column normalised through the grid exchange); without it
@@ -233,15 +235,22 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
     double* X = p.xs + (int64_t)blockIdx.x * 3 * T * ld;
     double* AC = X + (int64_t)T * ld;
     double* AD = AC + (int64_t)T * ld;
+    // Phase 3, two ways.  Many rows per CTA (C5: 13.5 K): as a look-ahead that builds only the
+    // next tile's accumulators (the far columns read, never rewritten: 35 instead of 61 GB at C5).
+    // Few rows (TDT2, K=480: 249): the per-tile read-modify-write of the later columns, whose
+    // (row, 4-column) items keep every thread busy (measured: 5.2 vs 5.9 ms per W update).
+    const bool narrow = nl < 2 * kSThreads;
     for (int b = 0; b < k; b += T) {
         const int e = (b + T < k) ? b + T : k, w = e - b;
         // ---- the tile, column-major: each warp transposes 32-row chunks through its own
-        // shared-memory stage (row segments in, coalesced 32-row column pieces out)
+        // shared-memory stage (row segments in, coalesced 32-row column pieces out).  The
+        // accumulators AC of tiles after the first were built by the previous tile's look-ahead.
         for (int64_t i0 = (int64_t)warp * kWarp; i0 < nl; i0 += (int64_t)kSWarps * kWarp) {
-            const double* src[3] = {p.old_m, p.nb, p.add};
-            double* dst[3] = {X, AC, AD};
+            const double* src[3] = {p.old_m, p.add, p.nb};
+            double* dst[3] = {X, AD, AC};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
+                if (a == 2 && b > 0 && !narrow) break;  // built by the previous tile's look-ahead
                 for (int idx = lane; idx < kWarp * w; idx += kWarp) {
                     const int ii = idx / w, j = idx - ii * w;
                     if (i0 + ii < nl) st[j * (kWarp + 1) + ii] = src[a][(r0 + i0 + ii) * k + b + j];
@@ -311,76 +320,78 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
                     X[tt * ld + i] = clamp_floor(p.eps, __ddiv_rn(X[tt * ld + i], norm));  // tiled.cpp:146
             }
         }
-        // ---- phase 3 (tiled.cpp:158-174): nb(r, c) += (-coeff(b+j, c)) * new(r, b+j), j ascending,
-        // for every c >= e.  One thread per row: the row's w new values (a coalesced column read of X)
-        // stay in registers for all its columns; the tile's coefficient rows are staged in shared
-        // memory (every thread reads the same entry: broadcast); 4 columns of the row per step
-        // (32-byte sector-sized accesses of the row-major factor).
-        if (e < k) {
-            const int rest = k - e;
-            for (int idx = tid; idx < w * rest; idx += kSThreads) {
-                const int j = idx / rest, c = idx - j * rest;
-                cq[j * rest + c] = -1.0 * p.coeff[(int64_t)(b + j) * k + e + c];
-            }
-            __syncthreads();
-            const bool vec4 = (k % 2 == 0) && (e % 2 == 0);
-            for (int64_t i = tid; i < nl; i += kSThreads) {
-                double x[16];
-                const bool small = w <= 16;
-                if (small) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) x[j] = (j < w) ? X[j * ld + i] : 0.0;
+        if (narrow) {
+            // ---- phase 3 (tiled.cpp:158-174): nb(r, c) += (-coeff(b+j, c)) * new(r, b+j), j ascending,
+            // for every c >= e.  One thread per row: the row's w new values (a coalesced column read of X)
+            // stay in registers for all its columns; the tile's coefficient rows are staged in shared
+            // memory (every thread reads the same entry: broadcast); 4 columns of the row per step
+            // (32-byte sector-sized accesses of the row-major factor).
+            if (e < k) {
+                const int rest = k - e;
+                for (int idx = tid; idx < w * rest; idx += kSThreads) {
+                    const int j = idx / rest, c = idx - j * rest;
+                    cq[j * rest + c] = -1.0 * p.coeff[(int64_t)(b + j) * k + e + c];
                 }
-                double* row = p.nb + (r0 + i) * k + e;
-                auto load4 = [&](int c0, double (&a)[4]) {
-                    if (c0 + 4 <= rest && vec4) {
-                        const double2 lo = *reinterpret_cast<const double2*>(row + c0);
-                        const double2 hi = *reinterpret_cast<const double2*>(row + c0 + 2);
-                        a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) a[u] = (c0 + u < rest) ? row[c0 + u] : 0.0;
-                    }
-                };
-                double an[4];
-                load4(0, an);
-                for (int c0 = 0; c0 < rest; c0 += 4) {
-                    double a[4];
-                    const bool full = c0 + 4 <= rest;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) a[u] = an[u];
-                    if (c0 + 4 < rest) load4(c0 + 4, an);  // the next group's loads in flight during this one
+                __syncthreads();
+                const bool vec4 = (k % 2 == 0) && (e % 2 == 0);
+                for (int64_t i = tid; i < nl; i += kSThreads) {
+                    double x[16];
+                    const bool small = w <= 16;
                     if (small) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            if (j < w) {
+                        for (int j = 0; j < 16; ++j) x[j] = (j < w) ? X[j * ld + i] : 0.0;
+                    }
+                    double* row = p.nb + (r0 + i) * k + e;
+                    auto load4 = [&](int c0, double (&a)[4]) {
+                        if (c0 + 4 <= rest && vec4) {
+                            const double2 lo = *reinterpret_cast<const double2*>(row + c0);
+                            const double2 hi = *reinterpret_cast<const double2*>(row + c0 + 2);
+                            a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) a[u] = (c0 + u < rest) ? row[c0 + u] : 0.0;
+                        }
+                    };
+                    double an[4];
+                    load4(0, an);
+                    for (int c0 = 0; c0 < rest; c0 += 4) {
+                        double a[4];
+                        const bool full = c0 + 4 <= rest;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) a[u] = an[u];
+                        if (c0 + 4 < rest) load4(c0 + 4, an);  // the next group's loads in flight during this one
+                        if (small) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                if (j < w) {
+                                    const double* q = cq + j * rest + c0;
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u)
+                                        if (c0 + u < rest) a[u] = M::madd(a[u], q[u], x[j]);
+                                }
+                            }
+                        } else {
+                            for (int j = 0; j < w; ++j) {
+                                const double xj = X[j * ld + i];
                                 const double* q = cq + j * rest + c0;
 #pragma unroll
                                 for (int u = 0; u < 4; ++u)
-                                    if (c0 + u < rest) a[u] = M::madd(a[u], q[u], x[j]);
+                                    if (c0 + u < rest) a[u] = M::madd(a[u], q[u], xj);
                             }
                         }
-                    } else {
-                        for (int j = 0; j < w; ++j) {
-                            const double xj = X[j * ld + i];
-                            const double* q = cq + j * rest + c0;
+                        if (full && vec4) {
+                            *reinterpret_cast<double2*>(row + c0) = make_double2(a[0], a[1]);
+                            *reinterpret_cast<double2*>(row + c0 + 2) = make_double2(a[2], a[3]);
+                        } else {
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
-                                if (c0 + u < rest) a[u] = M::madd(a[u], q[u], xj);
+                                if (c0 + u < rest) row[c0 + u] = a[u];
                         }
-                    }
-                    if (full && vec4) {
-                        *reinterpret_cast<double2*>(row + c0) = make_double2(a[0], a[1]);
-                        *reinterpret_cast<double2*>(row + c0 + 2) = make_double2(a[2], a[3]);
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (c0 + u < rest) row[c0 + u] = a[u];
                     }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
         // ---- the finished tile back to the row-major factor (the same warp-level transpose);
         // sharded: also into every other rank's window — the W all-gather fused into the update,
         // each tile's rows travelling over NVLink while the later tiles compute
@@ -402,6 +413,55 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_w_kernel(StreamArgs p) {
                 }
             }
             __syncwarp();
+        }
+        __syncthreads();
+        // ---- phase 3 as a look-ahead (tiled.cpp:158-174): phase 3 of every finished tile adds to
+        // the later columns in tile order; the next tile's columns are the only ones the next phase
+        // 2 reads, so they are built here — their phase-A values (in nb, never rewritten) plus the
+        // sum over kk < e of (-coeff(kk, c)) * new(r, kk), kk ascending: the reference's order —
+        // straight into the column-major AC.  The far columns are read, never rewritten.  One
+        // thread per row; the next tile's coefficient panel in shared memory (broadcast reads).
+        if (!narrow && e < k) {
+            const int bn = e, wn = (bn + T < k) ? T : k - bn;
+            for (int idx = tid; idx < e * wn; idx += kSThreads) {
+                const int kk = idx / wn, c = idx - kk * wn;
+                cq[kk * wn + c] = -1.0 * p.coeff[(int64_t)kk * k + bn + c];
+            }
+            __syncthreads();
+            for (int64_t i = tid; i < nl; i += kSThreads) {
+                const double* row = p.nb + (r0 + i) * k;
+                if (wn <= 16) {
+                    double a[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) a[c] = (c < wn) ? row[bn + c] : 0.0;
+                    for (int kk = 0; kk < e; ++kk) {
+                        const double xv = row[kk];
+                        const double* q = cq + kk * wn;
+#pragma unroll
+                        for (int c = 0; c < 16; ++c)
+                            if (c < wn) a[c] = M::madd(a[c], q[c], xv);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (c < wn) AC[c * ld + i] = a[c];
+                } else {
+                    for (int c0 = 0; c0 < wn; c0 += 8) {
+                        double a[8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) a[c] = (c0 + c < wn) ? row[bn + c0 + c] : 0.0;
+                        for (int kk = 0; kk < e; ++kk) {
+                            const double xv = row[kk];
+                            const double* q = cq + kk * wn + c0;
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                if (c0 + c < wn) a[c] = M::madd(a[c], q[c], xv);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            if (c0 + c < wn) AC[(c0 + c) * ld + i] = a[c];
+                    }
+                }
+            }
         }
         __syncthreads();
     }
