@@ -270,7 +270,8 @@ plnmf_status plnmf_gpu_set_product(plnmf_gpu_engine* e, plnmf_product which,
  * exchange data with each other on the device, over NVLink peer memory).
  * Factors and products crossing the boundary are the rank's local rows;
  * init_factors gives each rank its rows of the whole factors' stream
- * (proj/src/solver.cpp:43-51).  Tiled algorithm only; Math::exact or fused. */
+ * (proj/src/solver.cpp:43-51).  Both algorithms (the W update's column norms are
+ * exchanged between the ranks inside its kernel); Math::exact or fused. */
 typedef enum plnmf_buffer {
     PLNMF_BUF_W = 0,  /* local W rows, row-major (v_hi-v_lo) x K */
     PLNMF_BUF_HT = 1, /* local Ht rows, row-major (d_hi-d_lo) x K */

@@ -362,8 +362,27 @@ void update_w_reference_order(plnmf_gpu_engine* e, const plnmf_config& cfg, plnm
 // rows, every column's norm exchanged with the other ranks inside the kernel
 // (peer.cuh), then the new rows pushed into every rank's window.
 void update_w_shard(plnmf_gpu_engine* e, const plnmf_config& cfg, plnmf_algorithm alg) {
-    if (alg != PLNMF_ALGORITHM_TILED)
-        throw std::invalid_argument("sharded engine: the W update is sharded for the tiled algorithm only");
+    if (alg != PLNMF_ALGORITHM_TILED) {
+        // update_w_reference (hals.cpp:77-108) on the local rows, in place, every column's norm
+        // exchanged with the other ranks inside the persistent kernel; then the rows to every rank
+        if (!e->have_ref_w) {
+            e->plan_ref_w = kern::plan_reference_w(e->v, e->device);
+            if (e->sm_cap > 0 && e->sm_cap < e->plan_ref_w.grid) {  // ranks sharing one GPU
+                e->plan_ref_w.grid = e->sm_cap;
+                e->plan_ref_w.cooperative = false;
+                e->plan_ref_w.rows_per_cta = e->v > 0 ? (e->v + e->sm_cap - 1) / e->sm_cap : 1;
+            }
+            e->have_ref_w = true;
+        }
+        const plnmf::WorldXch x = plnmf::shard::next_exchange(e);
+        e->launches += kern::reference_update_w(e->s, e->math, e->plan_ref_w, e->v, e->k, cfg.epsilon, e->w, e->p,
+                                                e->q, e->norms, e->partials, e->counters, e->totals, &x);
+        e->update_macs += (uint64_t)e->v * e->k * (e->k + 3);
+        plnmf::shard::push_factor(e, plnmf::kChanW);
+        e->s_valid = false;
+        e->r_valid = false;
+        return;
+    }
     check_tile(cfg, e->k);
     ensure_plans(e, cfg.tile_size);
     const plnmf::WorldXch x = plnmf::shard::next_exchange(e);

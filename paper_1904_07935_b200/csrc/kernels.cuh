@@ -138,9 +138,10 @@ int64_t exchange_counters(int64_t k);
 int reference_update_h(cudaStream_t s, Math m, int64_t d, int64_t k, double eps, double* ht,
                        const double* r, const double* sm);
 PhaseBPlan plan_reference_w(int64_t v, int device);
+// xch (sharded engine, world > 1): every column norm summed over the ranks (peer.cuh).
 int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v, int64_t k,
                        double eps, double* w, const double* p, const double* q, double* norms,
-                       double* partials, unsigned* counters, double* totals);
+                       double* partials, unsigned* counters, double* totals, const WorldXch* xch = nullptr);
 
 // ---- reference-order reductions (Math::reference_order, refmode.cu) -------------------
 // *ss_out := column t's sum of squares of col_src (row-major n x k) in the

@@ -447,6 +447,7 @@ plnmf_status plnmf_gpu_shard_connect_local(plnmf_gpu_engine* const* engines, int
             // that all ranks' kernels are resident together (they wait on one another)
             if (one_device && world > 1) e->sm_cap = e->sms / world;
             e->plan_tile = -1;
+            e->have_ref_w = false;
             e->connected = true;
         }
     });

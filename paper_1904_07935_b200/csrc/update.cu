@@ -135,9 +135,10 @@ struct RefWArgs {
     double* partials;
     unsigned* counters;
     double* totals;
+    WorldXch xch;  // WORLD: the column norms span the ranks of a sharded engine (peer.cuh)
 };
 
-template <class M>
+template <class M, bool WORLD = false>
 __global__ void __launch_bounds__(kRefWThreads) ref_update_w_kernel(RefWArgs a) {
     __shared__ double red[48];
     const int k = a.k;
@@ -157,7 +158,9 @@ __global__ void __launch_bounds__(kRefWThreads) ref_update_w_kernel(RefWArgs a) 
         }
         const double blk = block_sum(ss, red);
         if (threadIdx.x < kWarp) {
-            const double nrm = grid_exchange(blk, kk, gridDim.x, a.partials, a.counters);
+            const double nrm =
+                WORLD ? __dsqrt_rn(world_sum(grid_exchange_sum(blk, kk, gridDim.x, a.partials, a.counters), kk, a.xch))
+                      : grid_exchange(blk, kk, gridDim.x, a.partials, a.counters);
             if (threadIdx.x == 0) red[40] = nrm;
         }
         __syncthreads();
@@ -382,14 +385,21 @@ PhaseBPlan plan_reference_w(int64_t v, int device) {
 
 int reference_update_w(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t v, int64_t k, double eps,
                        double* w, const double* p, const double* q, double* norms, double* partials,
-                       unsigned* counters, double* totals) {
+                       unsigned* counters, double* totals, const WorldXch* xch) {
     if (v <= 0 || k <= 0) return 0;
     exchange_reset(s, k, plan.grid, partials, counters);
-    RefWArgs a{v, (int)k, eps, plan.rows_per_cta, w, p, q, norms, partials, counters, totals};
+    const bool world = xch && xch->world > 1;
+    RefWArgs a{v, (int)k, eps, plan.rows_per_cta, w, p, q, norms, partials, counters, totals,
+               world ? *xch : WorldXch{}};
     void* args[] = {&a};
-    const void* fn = (m == Math::exact) ? (const void*)ref_update_w_kernel<MathExact>
-                                        : (const void*)ref_update_w_kernel<MathFused>;
-    PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3((unsigned)plan.grid), dim3(kRefWThreads), args, 0, s));
+    const bool ex = m == Math::exact;
+    const void* fn = world ? (ex ? (const void*)ref_update_w_kernel<MathExact, true>
+                                 : (const void*)ref_update_w_kernel<MathFused, true>)
+                           : (ex ? (const void*)ref_update_w_kernel<MathExact> : (const void*)ref_update_w_kernel<MathFused>);
+    if (plan.cooperative)
+        PLNMF_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3((unsigned)plan.grid), dim3(kRefWThreads), args, 0, s));
+    else  // ranks sharing one GPU: a share of the SMs, co-resident with the other ranks' kernels
+        PLNMF_CUDA_CHECK(cudaLaunchKernel(fn, dim3((unsigned)plan.grid), dim3(kRefWThreads), args, 0, s));
     return 1;
 }
 

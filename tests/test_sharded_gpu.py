@@ -145,6 +145,31 @@ def case_iterate_matches_single_engine(world):
         e.close()
 
 
+def case_fast_hals_sharded(world):
+    """The reference (fast-hals) algorithm on the sharded engine: update_w_reference's column
+    norms exchanged between the ranks inside its persistent kernel, H row-local."""
+    m, w0, ht0 = conditioned_state()
+    plan = ShardPlan(V, D, world)
+    cfg = P.SolverConfig(rank=K, max_iters=3, rel_tol=0.0)
+    single = P.Engine(P.InputMatrix(m), K)
+    single.set_factors(P.FactorPair(w0, ht0))
+    tr1 = single.iterate(cfg, P.Algorithm.reference)
+    f1 = single.get_factors()
+    engines = make_ranks(m, world)
+    on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*plan.v_range(g))],
+                                                              ht0[slice(*plan.d_range(g))])))
+    trs = on_ranks(engines, lambda e, g: e.iterate(cfg, P.Algorithm.reference))
+    for tr in trs[1:]:
+        assert [r.rel_error for r in tr.records] == [r.rel_error for r in trs[0].records]
+    for a, b in zip(trs[0].records, tr1.records):
+        assert abs(a.rel_error - b.rel_error) <= 1e-10 * b.rel_error
+    w = np.concatenate([e.get_factors().w for e in engines])
+    ht = np.concatenate([e.get_factors().ht for e in engines])
+    assert rel_max(f1.w, w) <= 1e-10 and rel_max(f1.ht, ht) <= 1e-10
+    for e in engines:
+        e.close()
+
+
 def case_generated_shards(world):
     """The C5 path: each rank generates its row block and its A^T block on the
     device; products from init_factors equal those of shards built from the
@@ -217,7 +242,8 @@ def case_ipc_rank(world):
 
 
 CASES = {f.__name__: f for f in (case_step_products_and_updates, case_iterate_matches_single_engine,
-                                  case_generated_shards, case_missing_rank_times_out, case_ipc_rank)}
+                                  case_fast_hals_sharded, case_generated_shards, case_missing_rank_times_out,
+                                  case_ipc_rank)}
 
 
 def _run_case(name, world):
@@ -235,6 +261,11 @@ def test_sharded_step_products_and_updates_match_the_restatement(gpu, world):
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_iterate_matches_single_engine(gpu, world):
     _run_case("case_iterate_matches_single_engine", world)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fast_hals_on_the_sharded_engine(gpu, world):
+    _run_case("case_fast_hals_sharded", world)
 
 
 @pytest.mark.parametrize("world", [2, 4])
