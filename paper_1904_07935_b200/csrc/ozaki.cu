@@ -236,24 +236,31 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(GemmArgs g) {
             }
         }
     } else if (warp == 1) {
-        // instruction descriptor: D s32, A/B u8 K-major, N = NT, M = 128
-        const uint32_t idesc = (2u << 4) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(kMT >> 4) << 24);
+        // For one A digit da, the B digits db = 1 .. S+1-da feed the levels L = da+1 .. S+1, whose
+        // accumulators sit side by side in TMEM ((L-2) * NT) while the B digit tiles sit side by
+        // side in shared memory: one MMA with N = (#db) * NT covers them all (split at N <= 256).
+        // 9 MMAs per k step instead of 21, and each A digit tile is read from shared memory once
+        // per group instead of once per pair — the same exact integer sums.
+        constexpr int kMaxDig = (256 / NT) < kS ? (256 / NT) : kS;  // B digit tiles per MMA
         for (int i = 0; i < nsteps; ++i) {
             const int s = i % kStages;
             mbar_wait(full + s, (i / kStages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
 #pragma unroll
-                for (int L = 2; L <= kS + 1; ++L) {
+                for (int da = 1; da <= kS; ++da) {
+                    const int nb = kS + 1 - da;  // db = 1 .. nb
 #pragma unroll
-                    for (int da = 1; da <= kS; ++da) {
-                        const int db = L - da;
-                        if (db < 1 || db > kS) continue;
+                    for (int d0 = 1; d0 <= nb; d0 += kMaxDig) {
+                        const int cnt = (nb - d0 + 1) < kMaxDig ? (nb - d0 + 1) : kMaxDig;
+                        // instruction descriptor: D s32, A/B u8 K-major, N = cnt * NT, M = 128
+                        const uint32_t idesc =
+                            (2u << 4) | ((uint32_t)((cnt * NT) >> 3) << 17) | ((uint32_t)(kMT >> 4) << 24);
                         const uint64_t ad = smem_desc(sA + s * kABytes + (da - 1) * kMT * kKStep);
-                        const uint64_t bd = smem_desc(sB + s * kBBytes + (db - 1) * NT * kKStep);
-                        // the first product of each level at the first k step initialises its accumulator
-                        const uint32_t acc = (i > 0 || da > ((L - kS) > 1 ? (L - kS) : 1)) ? 1u : 0u;
-                        mma_u8(tmem + (uint32_t)((L - 2) * NT), ad, bd, idesc, acc);
+                        const uint64_t bd = smem_desc(sB + s * kBBytes + (d0 - 1) * NT * kKStep);
+                        // da = 1 is the first digit of every level: at the first k step it initialises
+                        const uint32_t acc = (i > 0 || da > 1) ? 1u : 0u;
+                        mma_u8(tmem + (uint32_t)((da + d0 - 2) * NT), ad, bd, idesc, acc);
                     }
                 }
                 mma_commit(empty + s);  // the stage's smem is free once these MMAs have read it
