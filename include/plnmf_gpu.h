@@ -306,7 +306,8 @@ plnmf_status plnmf_gpu_shard_ipc_handle(plnmf_gpu_engine* e, void* handle);
 plnmf_status plnmf_gpu_shard_connect(plnmf_gpu_engine* e, const void* handles);
 /* Connecting the ranks 0..world-1 of one process (any devices with peer access; several
  * ranks may share one device, each then using an equal share of its SMs — that needs
- * CUDA_MODULE_LOADING=EAGER in the process, else PLNMF_INVALID_ARGUMENT). */
+ * CUDA_MODULE_LOADING=EAGER in the process, else PLNMF_INVALID_ARGUMENT).  The ranks use
+ * each other's windows directly: destroy them together, after their last call. */
 plnmf_status plnmf_gpu_shard_connect_local(plnmf_gpu_engine* const* engines, int32_t world);
 /* Failure detection: a device-side wait for another rank gives up after `seconds`
  * (default 20) and the next synchronising call on this rank fails with PLNMF_CUDA

@@ -165,7 +165,8 @@ def connect(engine: ShardEngine, group=None, chain_norm: bool = True) -> None:
 
 def connect_local(engines: Sequence[ShardEngine], chain_norm: bool = False) -> None:
     """Connects the ranks 0..world-1 held by this process (several ranks on one
-    GPU share its SMs; several GPUs need peer access)."""
+    GPU share its SMs and need CUDA_MODULE_LOADING=EAGER; several GPUs need peer
+    access).  The ranks then use each other's windows: close them together."""
     arr = (C.c_void_p * len(engines))(*[e._h for e in engines])
     _check(L.lib().plnmf_gpu_shard_connect_local(arr, len(engines)))
     if chain_norm:
