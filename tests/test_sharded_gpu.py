@@ -69,6 +69,9 @@ def case_step_products_and_updates(world):
     vr = [plan.v_range(g) for g in range(world)]
     dr = [plan.d_range(g) for g in range(world)]
     engines = make_ranks(m, world, K)
+    if world == 3:  # the column-blocked SpMM on the padded window rows (small blocks, many passes)
+        for e in engines:
+            e.force_spmm_blocks(97)
     on_ranks(engines, lambda e, g: e.set_factors(P.FactorPair(w0[slice(*vr[g])], ht0[slice(*dr[g])])))
     cfg = P.SolverConfig(rank=K, tile_size=TILE)
     trp, tci, tval = R.transpose(V, D, m.row_ptr, m.col_idx, m.values)
