@@ -168,37 +168,66 @@ namespace plnmf {
 // 16-lane half and the coefficient load is one conflict-free wavefront) and up
 // to RG rows g, g + ng, g + 2 ng, ... (ng = count / 16 row groups).
 // Per-element order as lookahead_gemm_private: bit-identical under Math::exact.
+template <int OFF>
+__device__ __forceinline__ double lds64_at(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+
 template <class M, int RG>
 __device__ __forceinline__ void lookahead_gemm_resident(const GemmArgs& g, const double* resid, int ld) {
     const int wn = g.en - g.bn, k = g.k;
     const int ng = g.count / 16;  // row groups
     const int c = g.self % 16, grp = g.self / 16;
-    if (c >= wn || grp >= ng) return;
+    if (c >= wn || grp >= ng || grp >= g.nrows) return;
     const unsigned qb = smem_u32(g.q), xb = smem_u32(resid);
+    // rows past the block recompute the last row (no predicates in the loop);
+    // only the first rn are stored
     int rr[RG];
     int rn = 0;
 #pragma unroll
     for (int i = 0; i < RG; ++i) {
-        rr[i] = grp + i * ng;
-        if (rr[i] < g.nrows) rn = i + 1;
+        const int r = grp + i * ng;
+        if (r < g.nrows) rn = i + 1;
+        rr[i] = min(r, g.nrows - 1);
     }
-    if (rn == 0) return;
     double a[RG];
 #pragma unroll
     for (int i = 0; i < RG; ++i) {
-        a[i] = 0.0;
-        if (i < rn) {
-            const double o = resid[rr[i] * ld + g.bn + c];
-            a[i] = g.use_diag ? dmul(o, lds64(qb + 8u * ((g.bn + c) * g.tq + c))) : o;
-        }
+        const double o = resid[rr[i] * ld + g.bn + c];
+        a[i] = g.use_diag ? dmul(o, lds64(qb + 8u * ((g.bn + c) * g.tq + c))) : o;
     }
+    // addresses advance by increments; the row operands of 4 consecutive kk
+    // are immediate offsets from one base
+    const unsigned qs = 8u * g.tq, qs2 = 2u * qs, qs3 = 3u * qs, qs4 = 4u * qs;
     auto seg = [&](int k0, int k1) {
-#pragma unroll 4
-        for (int kk = k0; kk < k1; ++kk) {
-            const double q = -1.0 * lds64(qb + 8u * (kk * g.tq + c));
+        unsigned qa = qb + 8u * (k0 * g.tq + c);
+        unsigned xa[RG];
 #pragma unroll
-            for (int i = 0; i < RG; ++i)
-                if (i < rn) a[i] = M::madd(a[i], q, lds64(xb + 8u * (rr[i] * ld + kk)));
+        for (int i = 0; i < RG; ++i) xa[i] = xb + 8u * (rr[i] * ld + k0);
+        int n = k1 - k0;
+        for (; n >= 4; n -= 4) {
+            const double q0 = -1.0 * lds64(qa), q1 = -1.0 * lds64(qa + qs), q2 = -1.0 * lds64(qa + qs2),
+                         q3 = -1.0 * lds64(qa + qs3);
+#pragma unroll
+            for (int i = 0; i < RG; ++i) {
+                a[i] = M::madd(a[i], q0, lds64_at<0>(xa[i]));
+                a[i] = M::madd(a[i], q1, lds64_at<8>(xa[i]));
+                a[i] = M::madd(a[i], q2, lds64_at<16>(xa[i]));
+                a[i] = M::madd(a[i], q3, lds64_at<24>(xa[i]));
+                xa[i] += 32u;
+            }
+            qa += qs4;
+        }
+        for (; n > 0; --n) {
+            const double q = -1.0 * lds64(qa);
+#pragma unroll
+            for (int i = 0; i < RG; ++i) {
+                a[i] = M::madd(a[i], q, lds64(xa[i]));
+                xa[i] += 8u;
+            }
+            qa += qs;
         }
     };
     seg(g.en, k);     // phase 1: old values of the columns right of the tile

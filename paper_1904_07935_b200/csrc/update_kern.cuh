@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     };
     auto build_next = [&](double* dst, int bn, int en, int bprev, int first, int count, int self) {
         const double* Q = Qn(bn);
-        if (TMAX > 0 && SQN && p.resident && count == nupd) {
+        if (TMAX > 0 && TMAX <= 16 && SQN && !NORMALIZE && p.resident && count == nupd) {  // planner: tile <= 16
             GemmArgs ga{dst, ldt, Qn(bn), TQ, bn, en, bprev, p.use_diag, p.old_m, p.out, r0, nrows, k, nullptr, 0,
                         count, self, 2};
             const int rg = (nrows + count / 16 - 1) / (count / 16);  // rows per thread (<= 4 by the planner)
