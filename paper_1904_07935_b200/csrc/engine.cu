@@ -167,16 +167,24 @@ int64_t operand_rows_h(const plnmf_gpu_engine* e) { return e->shard ? e->world *
 // R = A^T W then S = W^T W, one after the other on the engine stream (S is
 // skipped when the last error evaluation already left gram(W) in S: same W,
 // same deterministic kernel, same bits — the reference recomputes it,
-// proj/src/solver.cpp:34 vs proj/src/hals.cpp:31).  The two kernels are not
-// run concurrently: the SpMM is L2-gather bound and wants every SM's
-// registers for its loads in flight, the Gram is FP64-latency bound and
-// wants its own warps; side by side on two streams they took longer than
-// back to back (measured on the B200 at C2: P || Q 282 us vs P; Q 219 us).
+// proj/src/solver.cpp:34 vs proj/src/hals.cpp:31).  With an error evaluation
+// every iteration both come from evaluate_error_launch (the Gram first, then
+// R ahead on s2 in the registers the Gram leaves, see precompute_w).
 void precompute_h(plnmf_gpu_engine* e) {
     if (e->r_valid) {  // R was computed ahead, next to the last error evaluation
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join_r, 0));
         std::swap(e->r, e->r_next);
         e->r_valid = false;
+    } else if (e->sparse && !e->shard && !e->s_valid) {  // S first, R beside it (as in precompute_w)
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+        e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
+        e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r, e->nnz_t,
+                                      operand_rows_w(e), e->cursor_r, e->spmm_block, true);
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
+        e->s_valid = true;
+        return;
     } else if (e->sparse) {
         const double* w = e->w;
         if (e->shard) {  // every rank's W rows have arrived in this rank's window
@@ -196,8 +204,22 @@ void precompute_h(plnmf_gpu_engine* e) {
     e->s_valid = true;
 }
 
-// P = A Ht then Q = Ht^T Ht (the Gram scratch is shared with S).
+// P = A Ht and Q = Ht^T Ht (the Gram scratch is shared with S).
 void precompute_w(plnmf_gpu_engine* e) {
+    if (e->sparse && !e->shard) {
+        // Q first: its one wave of CTAs leaves each SM a quarter of its
+        // registers, where the 64-register SpMM runs alongside (P || Q 188 us vs
+        // P; Q 232 us at C2).  Launched the other way round, the SpMM's CTAs take
+        // every register and the two serialise.
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+        e->launches += kern::gram(e->s, e->math, e->d, e->k, e->ht, e->q, e->gram_scratch, e->sms);
+        e->launches += kern::spmm_csr(e->s2, e->math, e->v, e->rp, e->ci, e->val, e->ht, e->k, e->p, e->nnz,
+                                      operand_rows_h(e), e->cursor_p, e->spmm_block, true);
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->join, e->s2));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join, 0));
+        return;
+    }
     if (e->sparse) {
         const double* ht = e->ht;
         if (e->shard) {
@@ -487,7 +509,7 @@ void evaluate_error_launch(plnmf_gpu_engine* e, bool ahead_r, cudaEvent_t done) 
         PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
         PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
         e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next, e->nnz_t,
-                                      operand_rows_w(e), e->cursor_r, e->spmm_block);
+                                      operand_rows_w(e), e->cursor_r, e->spmm_block, true);  // next to the Gram
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
         e->r_valid = true;
     }

@@ -34,9 +34,10 @@ namespace kern {
 // nnz: the matrix's nonzero count (selects the unroll depth; -1 if unknown).
 // x_rows, cursor (rows int64 of workspace): an operand much larger than L2 is
 // processed in column blocks of spmm_block_rows(k) operand rows (bit-identical).
+// lean: a 64-register variant (same order) that fits next to a running Gram.
 int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
              const double* val, const double* x, int64_t k, double* y, int64_t nnz = -1, int64_t x_rows = -1,
-             int64_t* cursor = nullptr, int64_t force_block = 0);
+             int64_t* cursor = nullptr, int64_t force_block = 0, bool lean = false);
 int64_t spmm_block_rows(int64_t k);
 
 // g := m^T m (k x k) for row-major m (n x k), in the reference's compiled

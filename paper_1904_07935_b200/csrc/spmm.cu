@@ -257,9 +257,12 @@ void launch_blocked(cudaStream_t s, int nc2, int64_t rows, const int64_t* rp, co
 
 template <class M>
 void launch_pass_v2(cudaStream_t s, int nc2, int64_t rows, const int64_t* rp, const int32_t* ci,
-                    const double* val, const double* x, int64_t k, double* y, int col0, int ncols, bool short_rows) {
+                    const double* val, const double* x, int64_t k, double* y, int col0, int ncols, bool short_rows,
+                    bool lean) {
     const dim3 grid((unsigned)((rows + kSpmmThreads / kWarp - 1) / (kSpmmThreads / kWarp)));
-    if (nc2 == 4 && short_rows) {
+    if (nc2 == 4 && lean) {
+        spmm_csr_v2_kernel<4, M, 2, 4><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols);
+    } else if (nc2 == 4 && short_rows) {
         spmm_csr_v2_kernel<4, M, 2, 3><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols);
     } else {
         switch (nc2) {
@@ -317,7 +320,7 @@ int64_t spmm_block_rows(int64_t k) {
 
 int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int32_t* ci,
              const double* val, const double* x, int64_t k, double* y, int64_t nnz, int64_t x_rows,
-             int64_t* cursor, int64_t force_block) {
+             int64_t* cursor, int64_t force_block, bool lean) {
     if (rows <= 0 || k <= 0) return 0;
     // an operand much larger than L2: column-blocked passes (bit-identical, see spmm_blocked_kernel)
     const int64_t block = force_block > 0 ? force_block : spmm_block_rows(k);
@@ -349,8 +352,8 @@ int spmm_csr(cudaStream_t s, Math m, int64_t rows, const int64_t* rp, const int3
                          reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0;
         if (vec) {
             const int nc2 = (ncols + 2 * kWarp - 1) / (2 * kWarp);
-            if (m == Math::exact) launch_pass_v2<MathExact>(s, nc2, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows);
-            else launch_pass_v2<MathFused>(s, nc2, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows);
+            if (m == Math::exact) launch_pass_v2<MathExact>(s, nc2, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows, lean);
+            else launch_pass_v2<MathFused>(s, nc2, rows, rp, ci, val, x, k, y, (int)c0, ncols, short_rows, lean);
             ++launches;
             continue;
         }
