@@ -260,10 +260,11 @@ void launch_pass_v2(cudaStream_t s, int nc2, int64_t rows, const int64_t* rp, co
                     const double* val, const double* x, int64_t k, double* y, int col0, int ncols, bool short_rows,
                     bool lean) {
     const dim3 grid((unsigned)((rows + kSpmmThreads / kWarp - 1) / (kSpmmThreads / kWarp)));
-    if (nc2 == 4 && lean) {
+    // 64 registers (4 CTAs, 32 warps per SM): beside a running Gram (lean), and
+    // for short rows on its own (A*Ht at C2: 115 vs 125 us for the 80-register
+    // 3-CTA variant; A^T*W's longer rows run the same on the 4-deep unroll)
+    if (nc2 == 4 && (lean || short_rows)) {
         spmm_csr_v2_kernel<4, M, 2, 4><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols);
-    } else if (nc2 == 4 && short_rows) {
-        spmm_csr_v2_kernel<4, M, 2, 3><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols);
     } else {
         switch (nc2) {
             case 1: spmm_csr_v2_kernel<1, M><<<grid, kSpmmThreads, 0, s>>>(rows, rp, ci, val, x, k, y, k, col0, ncols); break;
