@@ -480,6 +480,56 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
                 }
             }
             mark(kProfChain);
+        } else if (is_chain && TMAX > 0 && !NORMALIZE) {
+            // ---- H phase 2, register-resident rows, latency-ordered: column tt's scratch
+            // sum is the reference's sequence 0 + new_0 c(0,tt) + ... + new_{tt-1} c(tt-1,tt)
+            // + old_tt c(tt,tt) + ... (tiled.cpp:118-131).  Its first tt-1 terms depend only
+            // on finished columns, so they are summed (P) while column tt-1 is still in
+            // flight; after new_{tt-1} only its own term and the old terms remain.
+            constexpr int TM = TMAX > 0 ? TMAX : 1;
+            const int r = ctid;
+            const bool own = r < nrows;
+            double x[TM];
+            double* arow = A + r * ldt;
+            const double* addr = p.add + (r0 + r) * k + b;
+            const double* orow = p.resident ? resid + r * p.ldr + b
+                                 : STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+#pragma unroll
+            for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
+            double pre = 0.0;  // sum_{j < tt-1} new_j c(j, tt), from 0
+            double add_next = b == 0 ? (own ? addr[0] : 0.0) : add_carry;
+#pragma unroll
+            for (int tt = 0; tt < TM; ++tt) {
+                if (tt < w) {
+                    double val = 0.0;
+                    const double add_t = add_next;
+                    if (own && tt + 1 < w) add_next = addr[tt + 1];
+                    if (own && tt + 1 == w && has_next) add_carry = addr[w];
+                    if (own) {
+                        double s = tt == 0 ? 0.0 : M::madd(pre, x[tt - 1], sqc[(tt - 1) * T + tt]);
+#pragma unroll
+                        for (int j = 0; j < TM; ++j)
+                            if (j >= tt && j < w) s = M::madd(s, x[j], sqc[j * T + tt]);
+                        if (tt + 1 < w) {  // the next column's prefix: new terms j < tt
+                            double pn = 0.0;
+#pragma unroll
+                            for (int j = 0; j < TM; ++j)
+                                if (j < tt) pn = M::madd(pn, x[j], sqc[j * T + tt + 1]);
+                            pre = pn;
+                        }
+                        val = clamp_floor(p.eps, dsub(dadd(arow[tt], add_t), s));
+                    }
+                    x[tt] = val;
+                    if (own) arow[tt] = val;
+                }
+            }
+            named_sync(1, nchain);
+            for (int idx = ctid; idx < nrows * w; idx += nchain) {
+                const int rr = idx / w, j = idx % w;
+                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+                if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
+            }
+            mark(kProfChain);
         } else if (is_chain && TMAX > 0) {
             // ---- phase 2 of this tile, register-resident rows (one row per row thread)
             constexpr int TM = TMAX > 0 ? TMAX : 1;
