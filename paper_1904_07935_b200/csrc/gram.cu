@@ -59,7 +59,9 @@ __host__ __device__ constexpr bool below_diag(int i, int j) {
     return (32 / TI) * i > (32 / TJ - 1) + (32 / TJ) * j;
 }
 
-template <class M, int TJ, int TI, bool DIAG>
+// JN (<= TJ): entries along b actually computed — TJ / 2 for a ragged last tile whose
+// valid columns (k - b0 <= 16) all lie in the first half (K = 240: tile 7 holds 16)
+template <class M, int TJ, int TI, bool DIAG, int JN = TJ>
 __device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __restrict__ m, double* __restrict__ part,
                                           int ta, int tb, double (&As)[2][32][32], double (&Bs)[2][32][32]);
 
@@ -75,11 +77,17 @@ __global__ void __launch_bounds__((32 / TI) * (32 / TJ), 8) gram_block_kernel(in
     __shared__ __align__(16) double Bs[2][kGramChunk][kGramTile];
     int ta, tb;
     decode_upper(blockIdx.x, ntile, ta, tb);
-    if (ta == tb) gram_tile<M, TJ, TI, true>(n, k, m, part, ta, tb, As, Bs);
-    else gram_tile<M, TJ, TI, false>(n, k, m, part, ta, tb, As, Bs);
+    const bool half_b = tb * kGramTile + 16 >= k;  // columns b0 + 16 .. b0 + 31 are all >= k
+    if (ta == tb) {
+        if (half_b) gram_tile<M, TJ, TI, true, TJ / 2>(n, k, m, part, ta, tb, As, Bs);
+        else gram_tile<M, TJ, TI, true>(n, k, m, part, ta, tb, As, Bs);
+    } else {
+        if (half_b) gram_tile<M, TJ, TI, false, TJ / 2>(n, k, m, part, ta, tb, As, Bs);
+        else gram_tile<M, TJ, TI, false>(n, k, m, part, ta, tb, As, Bs);
+    }
 }
 
-template <class M, int TJ, int TI, bool DIAG>
+template <class M, int TJ, int TI, bool DIAG, int JN>
 __device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __restrict__ m, double* __restrict__ part,
                                           int ta, int tb, double (&As)[2][32][32], double (&Bs)[2][32][32]) {
     const int64_t blk = blockIdx.y >> 1;
@@ -150,21 +158,21 @@ __device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __rest
 #pragma unroll
                     for (int i = 0; i < TI; ++i) av[h][i] = Ac[rr + h][ty + NY * i];
 #pragma unroll
-                    for (int j = 0; j < TJ; ++j) bv[h][j] = Bc[rr + h][tx + NX * j];
+                    for (int j = 0; j < JN; ++j) bv[h][j] = Bc[rr + h][tx + NX * j];
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < TJ; ++j)
+                        for (int j = 0; j < JN; ++j)
                             if (!(DIAG && below_diag<TJ, TI>(i, j))) pr[h][i][j] = dmul(av[h][i], bv[h][j]);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int i = 0; i < TI; ++i)
 #pragma unroll
-                        for (int j = 0; j < TJ; ++j)
+                        for (int j = 0; j < JN; ++j)
                             if (!(DIAG && below_diag<TJ, TI>(i, j))) acc[i][j] = dadd(acc[i][j], pr[h][i][j]);
             }
         }
@@ -173,11 +181,11 @@ __device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __rest
 #pragma unroll
             for (int i = 0; i < TI; ++i) av[i] = Ac[rr][ty + NY * i];
 #pragma unroll
-            for (int j = 0; j < TJ; ++j) bv[j] = Bc[rr][tx + NX * j];
+            for (int j = 0; j < JN; ++j) bv[j] = Bc[rr][tx + NX * j];
 #pragma unroll
             for (int i = 0; i < TI; ++i)
 #pragma unroll
-                for (int j = 0; j < TJ; ++j)
+                for (int j = 0; j < JN; ++j)
                     if (!(DIAG && below_diag<TJ, TI>(i, j))) acc[i][j] = M::madd(acc[i][j], av[i], bv[j]);
         }
         __syncthreads();
@@ -186,7 +194,7 @@ __device__ __forceinline__ void gram_tile(int64_t n, int k, const double* __rest
 #pragma unroll
     for (int i = 0; i < TI; ++i)
 #pragma unroll
-        for (int j = 0; j < TJ; ++j) {
+        for (int j = 0; j < JN; ++j) {
             const int a = a0 + ty + NY * i, b = b0 + tx + NX * j;
             if (a < k && b < k) pb[(int64_t)a * k + b] = acc[i][j];
         }
