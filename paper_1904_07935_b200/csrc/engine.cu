@@ -483,10 +483,10 @@ ErrorReport direct_error(plnmf_gpu_engine* e) {
 }
 
 // evaluate_error, proj/src/solver.cpp:32-39
-// ahead_r: also start the next iteration's R = A^T W on the side stream once
-// gram(W) is done, next to the error reductions and the host round trip
-// (measured: 1.83 ms/iteration vs 1.87 with R beside the Gram and 1.85 with R
-// after the reductions).
+// ahead_r: also start the next iteration's R = A^T W on the side stream, beside
+// gram(W) and then the error reductions and the host round trip (round 2, the
+// 64-register SpMM: e2e 702 -> 704 it/s against R started after the Gram; with
+// the earlier 80-register SpMM beside the Gram was slower, 1.87 vs 1.83 ms).
 // evaluate_error in two halves: launch (the kernels and the asynchronous readback of the
 // 3-double report, completion recorded in `done`) and finish (read it after `done`; the
 // direct fallback below 1e-6).  iterate() queues work between the two.
@@ -502,14 +502,19 @@ ErrorReport evaluate_error(plnmf_gpu_engine* e, bool ahead_r = false) {
 void evaluate_error_launch(plnmf_gpu_engine* e, bool ahead_r, cudaEvent_t done) {
     if (e->a2 == 0.0) throw plnmf::DomainError("relative_error_gram: zero input norm");
     if (!(e->a2 == e->a2)) throw std::invalid_argument("sharded engine: ||A||^2 not set (plnmf_gpu_shard_set_norm_sq)");
+    // R ahead: forked before the Gram so that it runs beside it (the Gram's CTAs
+    // are dispatched first; the 64-register SpMM takes the registers its wave
+    // leaves, as in precompute_w), then beside the error dots
+    if (ahead_r) {
+        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
+        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
+    }
     e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
     if (e->shard) plnmf::shard::reduce_kxk(e, plnmf::kChanS, e->sm);
     e->s_valid = true;
     if (ahead_r) {
-        PLNMF_CUDA_CHECK(cudaEventRecord(e->fork, e->s));
-        PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s2, e->fork, 0));
         e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next, e->nnz_t,
-                                      operand_rows_w(e), e->cursor_r, e->spmm_block, true);  // next to the Gram
+                                      operand_rows_w(e), e->cursor_r, e->spmm_block, true);
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
         e->r_valid = true;
     }
