@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
 #include "exchange.cuh"
@@ -486,49 +487,57 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             // + old_tt c(tt,tt) + ... (tiled.cpp:118-131).  Its first tt-1 terms depend only
             // on finished columns, so they are summed (P) while column tt-1 is still in
             // flight; after new_{tt-1} only its own term and the old terms remain.
-            constexpr int TM = TMAX > 0 ? TMAX : 1;
-            const int r = ctid;
-            const bool own = r < nrows;
-            double x[TM];
-            double* arow = A + r * ldt;
-            const double* addr = p.add + (r0 + r) * k + b;
-            const double* orow = p.resident ? resid + r * p.ldr + b
-                                 : STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
+            // full 16-wide tiles get their own copy with the width and the coefficient
+            // stride as constants (no predicates on the terms, immediate-offset loads)
+            auto hchain = [&](auto wconst) {
+                constexpr int WF = decltype(wconst)::value;
+                const int wl = WF > 0 ? WF : w, Tl = WF > 0 ? WF : T;
+                constexpr int TM = TMAX > 0 ? TMAX : 1;
+                const int r = ctid;
+                const bool own = r < nrows;
+                double x[TM];
+                double* arow = A + r * ldt;
+                const double* addr = p.add + (r0 + r) * k + b;
+                const double* orow = p.resident ? resid + r * p.ldr + b
+                                     : STAGE ? oldB[cur] + r * ldt : p.old_m + (r0 + r) * k + b;
 #pragma unroll
-            for (int j = 0; j < TM; ++j) x[j] = (own && j < w) ? orow[j] : 0.0;
-            double pre = 0.0;  // sum_{j < tt-1} new_j c(j, tt), from 0
-            double add_next = b == 0 ? (own ? addr[0] : 0.0) : add_carry;
+                for (int j = 0; j < TM; ++j) x[j] = (own && j < wl) ? orow[j] : 0.0;
+                double pre = 0.0;  // sum_{j < tt-1} new_j c(j, tt), from 0
+                double add_next = b == 0 ? (own ? addr[0] : 0.0) : add_carry;
 #pragma unroll
-            for (int tt = 0; tt < TM; ++tt) {
-                if (tt < w) {
-                    double val = 0.0;
-                    const double add_t = add_next;
-                    if (own && tt + 1 < w) add_next = addr[tt + 1];
-                    if (own && tt + 1 == w && has_next) add_carry = addr[w];
-                    if (own) {
-                        double s = tt == 0 ? 0.0 : M::madd(pre, x[tt - 1], sqc[(tt - 1) * T + tt]);
-#pragma unroll
-                        for (int j = 0; j < TM; ++j)
-                            if (j >= tt && j < w) s = M::madd(s, x[j], sqc[j * T + tt]);
-                        if (tt + 1 < w) {  // the next column's prefix: new terms j < tt
-                            double pn = 0.0;
+                for (int tt = 0; tt < TM; ++tt) {
+                    if (tt < wl) {
+                        double val = 0.0;
+                        const double add_t = add_next;
+                        if (own && tt + 1 < wl) add_next = addr[tt + 1];
+                        if (own && tt + 1 == wl && has_next) add_carry = addr[wl];
+                        if (own) {
+                            double s = tt == 0 ? 0.0 : M::madd(pre, x[tt - 1], sqc[(tt - 1) * Tl + tt]);
 #pragma unroll
                             for (int j = 0; j < TM; ++j)
-                                if (j < tt) pn = M::madd(pn, x[j], sqc[j * T + tt + 1]);
-                            pre = pn;
+                                if (j >= tt && j < wl) s = M::madd(s, x[j], sqc[j * Tl + tt]);
+                            if (tt + 1 < wl) {  // the next column's prefix: new terms j < tt
+                                double pn = 0.0;
+#pragma unroll
+                                for (int j = 0; j < TM; ++j)
+                                    if (j < tt) pn = M::madd(pn, x[j], sqc[j * Tl + tt + 1]);
+                                pre = pn;
+                            }
+                            val = clamp_floor(p.eps, dsub(dadd(arow[tt], add_t), s));
                         }
-                        val = clamp_floor(p.eps, dsub(dadd(arow[tt], add_t), s));
+                        x[tt] = val;
+                        if (own) arow[tt] = val;
                     }
-                    x[tt] = val;
-                    if (own) arow[tt] = val;
                 }
-            }
-            named_sync(1, nchain);
-            for (int idx = ctid; idx < nrows * w; idx += nchain) {
-                const int rr = idx / w, j = idx % w;
-                p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
-                if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
-            }
+                named_sync(1, nchain);
+                for (int idx = ctid; idx < nrows * wl; idx += nchain) {
+                    const int rr = idx / wl, j = idx % wl;
+                    p.out[(r0 + rr) * k + b + j] = A[rr * ldt + j];
+                    if (p.resident) resid[rr * p.ldr + b + j] = A[rr * ldt + j];
+                }
+            };
+            if (TMAX >= 16 && w == 16 && T == 16) hchain(std::integral_constant<int, 16>{});
+            else hchain(std::integral_constant<int, 0>{});
             mark(kProfChain);
         } else if (is_chain && TMAX > 0) {
             // ---- phase 2 of this tile, register-resident rows (one row per row thread)
