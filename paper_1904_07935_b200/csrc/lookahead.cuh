@@ -175,6 +175,13 @@ __device__ __forceinline__ double lds64_at(unsigned a) {
     return v;
 }
 
+template <int OFF>
+__device__ __forceinline__ double2 lds128_at(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(OFF));
+    return v;
+}
+
 template <class M, int RG>
 __device__ __forceinline__ void lookahead_gemm_resident(const GemmArgs& g, const double* resid, int ld) {
     const int wn = g.en - g.bn, k = g.k;
@@ -207,6 +214,24 @@ __device__ __forceinline__ void lookahead_gemm_resident(const GemmArgs& g, const
 #pragma unroll
         for (int i = 0; i < RG; ++i) xa[i] = xb + 8u * (rr[i] * ld + k0);
         int n = k1 - k0;
+        if (((ld | k0) & 1) == 0) {
+            // 16-byte aligned rows: the row operands of 4 consecutive kk as two LDS.128
+            // (the look-ahead is shared-memory issue bound: ncu short_sb / mio stalls)
+            for (; n >= 4; n -= 4) {
+                const double q0 = -1.0 * lds64(qa), q1 = -1.0 * lds64(qa + qs), q2 = -1.0 * lds64(qa + qs2),
+                             q3 = -1.0 * lds64(qa + qs3);
+#pragma unroll
+                for (int i = 0; i < RG; ++i) {
+                    const double2 x01 = lds128_at<0>(xa[i]), x23 = lds128_at<16>(xa[i]);
+                    a[i] = M::madd(a[i], q0, x01.x);
+                    a[i] = M::madd(a[i], q1, x01.y);
+                    a[i] = M::madd(a[i], q2, x23.x);
+                    a[i] = M::madd(a[i], q3, x23.y);
+                    xa[i] += 32u;
+                }
+                qa += qs4;
+            }
+        }
         for (; n >= 4; n -= 4) {
             const double q0 = -1.0 * lds64(qa), q1 = -1.0 * lds64(qa + qs), q2 = -1.0 * lds64(qa + qs2),
                          q3 = -1.0 * lds64(qa + qs3);
