@@ -73,9 +73,10 @@ int64_t pl_kbuf(int64_t rows, int64_t k, int64_t tile, bool normalize) {
 size_t pl_smem(int64_t rows, int64_t k, int64_t tile, bool stage_ops, bool sqn_smem, int kc, int kst = 2,
                bool normalize = false) {
     const int64_t tq = (tile + 7) & ~int64_t(7);
-    const int64_t prods = (normalize && tile <= 32) ? rows * (tile + 1) : 0;  // W chain products (exact path)
+    const int64_t ldt = (tile + 1) | 1;  // the kernel's odd shared-memory row stride
+    const int64_t prods = (normalize && tile <= 32) ? rows * ldt : 0;  // W chain products (exact path)
     const int64_t rings = kc > 0 ? kst * pl_kbuf(rows, k, tile, normalize) * (kc + 2) : 0;
-    return sizeof(double) * (size_t)((stage_ops ? 4 : 2) * rows * (tile + 1) + (sqn_smem ? k * tq : 0) +
+    return sizeof(double) * (size_t)((stage_ops ? 4 : 2) * rows * ldt + (sqn_smem ? k * tq : 0) +
                                      tile * tile + 48 + 1 + rings + prods);
 }
 
@@ -247,7 +248,7 @@ PhaseBPlan plan_tiled_update(int64_t n, int64_t k, int64_t tile, bool normalize,
         // H: keep the CTA's rows resident in shared memory when they fit (no
         // staging, no oldB), up to 4 rows per look-ahead thread of a column
         const int64_t tq = (tile + 7) & ~int64_t(7);
-        const size_t smem = sizeof(double) * (size_t)(2 * rpc * (tile + 1) + k * tq + tile * tile + 48 + 1 +
+        const size_t smem = sizeof(double) * (size_t)(2 * rpc * ((tile + 1) | 1) + k * tq + tile * tile + 48 + 1 +
                                                       rpc * (k + 2));
         if (smem <= (size_t)max_smem && rpc <= 4 * (pl_nupd(rpc, false) / 16)) {
             plan.resident = 1;

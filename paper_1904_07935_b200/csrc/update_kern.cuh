@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
     long long* const pprof = kDebugKnobs ? p.prof : nullptr;
     const int overlap = kDebugKnobs ? p.overlap : 1;
     extern __shared__ double smem[];
-    const int T = p.tile, k = p.k, ldt = T + 1;
+    // tile rows in shared memory at an odd stride of doubles (T + 1, or T + 2 for odd T):
+    // one thread per row, so an even stride would put many lanes on one bank
+    const int T = p.tile, k = p.k, ldt = (T + 1) | 1;
     const int TQ = (T + 7) & ~7;  // sqn leading dimension: whole 8-column panels, 16-byte rows
     const int R = p.rows_per_cta;
     const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -365,9 +367,9 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
             constexpr int TM = TMAX > 0 ? TMAX : 1;
             const int r = ctid;
             const bool own = !is_xwarp && r < nrows;
-            // prod[j]: this row's products at a row stride of T + 1 doubles (odd: lanes' 64-bit
-            // accesses spread over the banks), so every j is an immediate offset from one base
-            double* prod = prodS + r * (T + 1);
+            // prod[j]: this row's products at the odd row stride ldt (lanes' 64-bit accesses
+            // spread over the banks), so every j is an immediate offset from one base
+            double* prod = prodS + r * ldt;
             double* arow = A + r * ldt;
             const double* addr = p.add + (r0 + r) * k + b;
             const double* orow = p.resident ? resid + r * p.ldr + b
