@@ -35,6 +35,7 @@ void release(plnmf_gpu_engine* e) {
     for (cudaEvent_t ev : e->events) cudaEventDestroy(ev);
     if (e->fork) cudaEventDestroy(e->fork);
     if (e->join_r) cudaEventDestroy(e->join_r);
+    if (e->join_pw) cudaEventDestroy(e->join_pw);
     if (e->err_done) cudaEventDestroy(e->err_done);
     if (e->join) cudaEventDestroy(e->join);
     if (e->s) cudaStreamDestroy(e->s);
@@ -62,6 +63,7 @@ void setup_common(plnmf_gpu_engine* e, int device, int64_t rank) {
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join_r, cudaEventDisableTiming));
+    PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->join_pw, cudaEventDisableTiming));
     PLNMF_CUDA_CHECK(cudaEventCreateWithFlags(&e->err_done, cudaEventDisableTiming));
 }
 
@@ -86,6 +88,7 @@ void alloc_workspace(plnmf_gpu_engine* e) {
     e->n_partials = kern::exchange_partials_doubles(k, 2 * e->sms);
     e->partials = dalloc<double>(e, e->n_partials);
     e->dot_partials = dalloc<double>(e, kern::kDotBlocks);
+    e->dot_partials2 = dalloc<double>(e, kern::kDotBlocks);
     e->scalars = dalloc<double>(e, 8);
     e->staging = dalloc<double>(e, std::max(std::max(v, d), k) * k);  // factors and K x K products
     e->counters = dalloc<unsigned>(e, kern::exchange_counters(k));
@@ -512,19 +515,29 @@ void evaluate_error_launch(plnmf_gpu_engine* e, bool ahead_r, cudaEvent_t done) 
     e->launches += kern::gram(e->s, e->math, e->v, e->k, e->w, e->sm, e->gram_scratch, e->sms);
     if (e->shard) plnmf::shard::reduce_kxk(e, plnmf::kChanS, e->sm);
     e->s_valid = true;
+    // <P, W> reads only P and W: with R ahead it runs on s2 as well, after the SpMM and beside
+    // the Gram, off the engine stream's critical path (its own partials buffer)
+    const bool pw_side = ahead_r && !e->ref_order && !e->shard;
     if (ahead_r) {
         e->launches += kern::spmm_csr(e->s2, e->math, e->d, e->trp, e->tci, e->tval, e->w, e->k, e->r_next, e->nnz_t,
                                       operand_rows_w(e), e->cursor_r, e->spmm_block, true);
         PLNMF_CUDA_CHECK(cudaEventRecord(e->join_r, e->s2));
         e->r_valid = true;
+        if (pw_side) {
+            e->launches += kern::dot(e->s2, e->math, e->v * e->k, e->p, e->w, e->dot_partials2, e->scalars + 0);
+            PLNMF_CUDA_CHECK(cudaEventRecord(e->join_pw, e->s2));
+        }
     }
     if (e->ref_order) {  // the reference's serial sums (metrics.cpp:104-115)
         e->launches += kern::serial_dot_colmajor(e->s, e->v, e->k, e->p, e->w, e->scalars + 0);
         e->launches += kern::serial_dot_colmajor(e->s, e->k, e->k, e->sm, e->q, e->scalars + 1);
     } else {
-        e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
-        if (e->shard) plnmf::shard::reduce_scalar(e, e->scalars + 0);  // <P, W> over all ranks' rows
+        if (!pw_side) {
+            e->launches += kern::dot(e->s, e->math, e->v * e->k, e->p, e->w, e->dot_partials, e->scalars + 0);
+            if (e->shard) plnmf::shard::reduce_scalar(e, e->scalars + 0);  // <P, W> over all ranks' rows
+        }
         e->launches += kern::dot(e->s, e->math, e->k * e->k, e->sm, e->q, e->dot_partials, e->scalars + 1);
+        if (pw_side) PLNMF_CUDA_CHECK(cudaStreamWaitEvent(e->s, e->join_pw, 0));
     }
     e->launches += kern::error_finalize(e->s, e->a2, e->scalars + 0, e->scalars + 1, e->scalars + 2);
     PLNMF_CUDA_CHECK(cudaMemcpyAsync(e->host_scalars + 2, e->scalars + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, e->s));

@@ -51,6 +51,8 @@ struct plnmf_gpu_engine {
     bool s_valid = false;  // sm == gram(w) of the current w
     bool r_valid = false;  // r == A^T w of the current w, computed ahead on s2 (iterate: join_r)
     cudaEvent_t join_r = nullptr;
+    double* dot_partials2 = nullptr;  // <P, W> on s2 beside gram(W) (evaluate_error_launch with R ahead)
+    cudaEvent_t join_pw = nullptr;
     cudaEvent_t err_done = nullptr;  // an error report's readback has landed (evaluate_error)
     uint64_t launches = 0, update_macs = 0;
     int64_t bytes = 0;
