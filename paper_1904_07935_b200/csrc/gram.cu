@@ -178,6 +178,7 @@ __global__ void gram_combine_kernel(int k, int64_t nblk, const double* __restric
     if (a > b) return;
     const int64_t kk = (int64_t)k * k;
     double s = 0.0;
+#pragma unroll 4  // the loads of 4 blocks in flight at once (the adds stay in block order)
     for (int64_t blk = 0; blk < nblk; ++blk) {
         const double lane0 = part[(2 * blk) * kk + (int64_t)a * k + b];
         const double lane1 = part[(2 * blk + 1) * kk + (int64_t)a * k + b];

@@ -282,7 +282,8 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                norms, partials, counters, totals, prof, knob("PLNMF_NO_OVERLAP") ? 0 : knob("PLNMF_SKIP_LOOKAHEAD") ? 2 : 1,
                nullptr, qpanel, plan.stage_ops ? 1 : 0, plan.sqn_smem ? 1 : 0, plan.kc, plan.kst, plan.kbuf,
                knob_int("PLNMF_DBG"), plan.resident, (int)k + 2};
-    {
+    const bool panel = !plan.sqn_smem || !w_update;  // the W kernel stages its panels from coeff
+    if (panel) {
         const int tq = (int)((tile + 7) & ~int64_t(7));
         qpanel_kernel<<<(unsigned)std::min<int64_t>(1024, (qpanel_doubles(k, tile) + 255) / 256), 256, 0, s>>>(
             (int)k, (int)tile, tq, coeff, qpanel);
@@ -355,7 +356,7 @@ int tiled_update(cudaStream_t s, Math m, const PhaseBPlan& plan, int64_t n, int6
                          "->phase-3 done %.0f, ->coeff block + sync %.0f, ->first value %.0f\n",
                          bs[0] / nb, bs[1] / nb, bs[2] / nb, bs[3] / nb, bs[4] / nb);
     }
-    return 2;  // qpanel_kernel + pl_update_kernel
+    return panel ? 2 : 1;  // (qpanel_kernel +) pl_update_kernel
 }
 
 int reference_update_h(cudaStream_t s, Math m, int64_t d, int64_t k, double eps, double* ht,

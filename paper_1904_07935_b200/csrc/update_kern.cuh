@@ -265,13 +265,37 @@ __global__ void __launch_bounds__(kLThreads, 1) pl_update_kernel(LookArgs p) {
         }
         (void)first;
     };
+    // the next tile's coefficient panel coeff(:, bn .. en), zero-padded to TQ columns; completed
+    // by the caller's cp_async_wait before its barrier.  W: staged straight from coeff (no
+    // panel-building launch before the latency-bound update); H: copied from the panel built
+    // by qpanel_kernel (whole 16-byte rows: the smaller code keeps the H kernel's registers)
     auto load_sqn = [&](int bn, int en, int self, int count) {
-        (void)en;
         if (!SQN) return;
-        const double* src = p.qpanel + (int64_t)(bn / T) * k * TQ;
-        // panel rows are whole 8-column groups: 16-byte cp.async, completed by
-        // the caller's cp_async_wait before its barrier
-        for (int idx = self; idx < k * TQ / 2; idx += count) cp_async16(sqn + 2 * idx, src + 2 * idx);
+        if (!NORMALIZE) {
+            const double* src = p.qpanel + (int64_t)(bn / T) * k * TQ;
+            for (int idx = self; idx < k * TQ / 2; idx += count) cp_async16(sqn + 2 * idx, src + 2 * idx);
+            cp_async_commit();
+            return;
+        }
+        const int wn = en - bn, hq = TQ / 2;
+        if (((k | bn) & 1) == 0) {  // 16-byte pieces
+            for (int idx = self; idx < k * hq; idx += count) {
+                const int kk = idx / hq, j = 2 * (idx - kk * hq);
+                double* dst = sqn + kk * TQ + j;
+                if (j + 1 < wn) {
+                    cp_async16(dst, p.coeff + (int64_t)kk * k + bn + j);
+                } else {
+                    dst[0] = j < wn ? p.coeff[(int64_t)kk * k + bn + j] : 0.0;
+                    dst[1] = 0.0;
+                }
+            }
+        } else {
+            for (int idx = self; idx < k * TQ; idx += count) {
+                const int kk = idx / TQ, j = idx - kk * TQ;
+                if (j < wn) cp_async8(sqn + idx, p.coeff + (int64_t)kk * k + bn + j);
+                else sqn[idx] = 0.0;
+            }
+        }
         cp_async_commit();
     };
     // the tile's T x T coefficient block: a sub-block of the staged panel
